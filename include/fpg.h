@@ -1,0 +1,150 @@
+/*
+ * fpg.h -- C ABI of the B200 fingerprint-filtered k-approximate dictionary scan.
+ *
+ * This is the drop-in boundary under the reference's C++ API
+ * (/root/reference/proj/include/fingerprints/, namespace `fingerprints`).  The
+ * reference has no FFI of its own; its "operator API" is the class
+ * FingerprintedDictionary (dictionary.hpp:47-125).  Each entry point below
+ * names the reference interface it replaces.  Plain pointers and sizes only:
+ * no CUDA or torch types cross this boundary, no C++ exceptions escape it.
+ * Every function returns FPG_OK (0) or a negative FPG_E* status; the message
+ * of the last failure on the calling thread is fpg_last_error().
+ *
+ * Strings are byte blobs plus n+1 uint64 offsets: string i is
+ * bytes[offsets[i], offsets[i+1]).  Word ids are input-order indices (as in
+ * the reference, dictionary.hpp:86,112), returned as uint32 (N < 2^32),
+ * rebased by the dictionary's id_base.
+ */
+#ifndef FPG_H
+#define FPG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FPG_ABI_VERSION 1
+
+/* status codes */
+#define FPG_OK 0
+#define FPG_EINVAL -1        /* std::invalid_argument in the reference */
+#define FPG_EUNSUPPORTED -2  /* valid for the reference, not built for the GPU (e.g. k > 1) */
+#define FPG_ECUDA -3         /* CUDA runtime failure (no device, OOM, launch error) */
+#define FPG_ENOMEM -4        /* host allocation failure */
+
+/* fingerprint.hpp:14 enum class Variant */
+#define FPG_OCCURRENCE 0
+#define FPG_OCCURRENCE_HALVED 1
+#define FPG_COUNT 2
+#define FPG_POSITION 3
+/* fingerprint.hpp:15 enum class Metric */
+#define FPG_HAMMING 0
+#define FPG_LEVENSHTEIN 1
+
+#define FPG_MAX_WORD_LEN 4096
+
+/* Scheme (fingerprint.hpp:57-162) plus the fingerprint width W, which the
+ * reference fixes at 16 (fingerprint.hpp:31).  W in {16, 32, 64}; the layout
+ * rules are the reference's with 16 replaced by W.  letters = LetterSet
+ * symbols in slot order (letter_model.hpp:60-87). */
+typedef struct {
+    int32_t variant;
+    int32_t width;
+    int32_t bits_per_count;     /* Scheme::count b (default 2, fingerprint.hpp:65) */
+    int32_t bits_per_position;  /* Scheme::position p (default 3, fingerprint.hpp:68) */
+    int32_t nletters;
+    uint8_t letters[64];
+} fpg_scheme;
+
+/* QueryOptions (dictionary.hpp:36-44) + a stats switch (the reference's
+ * QueryStats* argument being non-null, dictionary.hpp:66,75). */
+typedef struct {
+    int32_t metric;
+    int32_t k;                 /* GPU path supports k in {0, 1} */
+    int32_t use_filter;
+    int32_t length_prefilter;
+    int32_t want_stats;
+} fpg_query_options;
+
+/* Per-query QueryStats (dictionary.hpp:19-34), in this order. */
+#define FPG_STAT_COMPARED 0
+#define FPG_STAT_REJECTED_BY_LENGTH 1
+#define FPG_STAT_REJECTED_BY_FINGERPRINT 2
+#define FPG_STAT_VERIFIED 3
+#define FPG_STAT_MATCHES 4
+#define FPG_NSTATS 5
+
+/* Result of a batch: CSR over queries, matches ascending by word id within a
+ * query (the order query_into emits them, dictionary.hpp:86-114).  Owned by
+ * the library; release with fpg_result_free. */
+typedef struct {
+    uint64_t nq;
+    uint64_t total;       /* number of (query, word) matches */
+    uint64_t* offsets;    /* nq + 1 */
+    uint32_t* word_ids;   /* total */
+    uint64_t* stats;      /* FPG_NSTATS * nq, or NULL when want_stats == 0 */
+} fpg_result;
+
+typedef struct fpg_dict fpg_dict;
+typedef struct fpg_batch fpg_batch;
+
+const char* fpg_last_error(void);
+int fpg_abi_version(void);
+int fpg_device_count(int* count);
+
+/* Scheme ctor validation (fingerprint.hpp:150-156, :84-100; letter_model.hpp:64-70)
+ * and Scheme::letter_capacity generalised to W.  Returns capacity or FPG_EINVAL. */
+int fpg_letter_capacity(int32_t variant, int32_t width, int32_t b, int32_t p);
+int fpg_scheme_validate(const fpg_scheme* scheme);
+/* variant_supports (fingerprint.hpp:36-38): 1 if the variant filters `metric`. */
+int fpg_scheme_supports(const fpg_scheme* scheme, int32_t metric);
+
+/* FingerprintedDictionary(words, scheme) (dictionary.hpp:51-56): uploads the
+ * words, builds one fingerprint per word on the GPU and lays the collection
+ * out length-bucketed in HBM.  `devices`/`ndevices` shard the words into
+ * contiguous input-order ranges, one per entry (a device may repeat).
+ * `id_base` is added to every reported word id (external sharding). */
+int fpg_dict_create(const uint8_t* bytes, const uint64_t* offsets, uint64_t n,
+                    const fpg_scheme* scheme, const int32_t* devices, int32_t ndevices,
+                    uint64_t id_base, fpg_dict** out);
+int fpg_dict_destroy(fpg_dict* dict);
+/* FingerprintedDictionary::size() (dictionary.hpp:62) */
+int fpg_dict_size(const fpg_dict* dict, uint64_t* n);
+/* FingerprintedDictionary::prints() (dictionary.hpp:59): fingerprints in
+ * input order, zero-extended to 64 bits. */
+int fpg_dict_prints(const fpg_dict* dict, uint64_t* out);
+/* Seconds the construction took (upload + K1 + layout), like bench.hpp:118-120. */
+int fpg_dict_build_seconds(const fpg_dict* dict, double* seconds);
+
+/* build() (fingerprint.hpp:276-284) for n strings on one device. */
+int fpg_build_fingerprints(const uint8_t* bytes, const uint64_t* offsets, uint64_t n,
+                           const fpg_scheme* scheme, int32_t device, uint64_t* out);
+
+/* FingerprintedDictionary::query_into (dictionary.hpp:75-118) for a batch of
+ * nq queries from host buffers (H2D, scan, D2H inside).  FPG_EINVAL when
+ * use_filter and the scheme does not support the metric (dictionary.hpp:78-79). */
+int fpg_query_batch(fpg_dict* dict, const uint8_t* qbytes, const uint64_t* qoffsets, uint64_t nq,
+                    const fpg_query_options* opt, fpg_result* out);
+int fpg_result_free(fpg_result* res);
+
+/* Staged form of fpg_query_batch for device-resident measurement:
+ * upload (H2D) -> run (device only, async) -> sync -> download (D2H). */
+int fpg_batch_create(fpg_dict* dict, fpg_batch** out);
+int fpg_batch_destroy(fpg_batch* batch);
+int fpg_batch_upload(fpg_batch* batch, const uint8_t* qbytes, const uint64_t* qoffsets,
+                     uint64_t nq);
+int fpg_batch_run(fpg_batch* batch, const fpg_query_options* opt);
+int fpg_batch_download(fpg_batch* batch, fpg_result* out);
+/* Device time (ms) of the last run on shard `shard`: whole run and the
+ * filter+verify kernel alone (CUDA events on the launching stream), plus the
+ * executed comparisons (length-compatible pairs) and survivors of that run. */
+int fpg_batch_last_timing(const fpg_batch* batch, int32_t shard, double* run_ms,
+                          double* filter_ms, uint64_t* executed_pairs, uint64_t* survivors,
+                          uint64_t* kernel_launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

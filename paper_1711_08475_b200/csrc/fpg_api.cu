@@ -1,0 +1,884 @@
+// fpg_api.cu -- C ABI (include/fpg.h) over the sm_100a kernels.
+//
+// Host runtime: per-device shards of the dictionary (contiguous input-order
+// id ranges, dictionary.hpp:51-56 keeps input order), per-batch device
+// scratch, tile planning over (query length, word length) bucket pairs, and
+// the host-side CSR merge across shards.  No compute happens on the host:
+// fingerprints, filtering, verification, ordering and CSR construction all
+// run on the GPU; the host only plans tiles from bucket counts, turns the
+// per-query survivor counts into QueryStats and concatenates shard rows.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <type_traits>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "../../include/fpg.h"
+#include "fpg_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(x)                                                                                  \
+    do {                                                                                       \
+        cudaError_t e_ = (x);                                                                  \
+        if (e_ != cudaSuccess)                                                                 \
+            throw Error(FPG_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_) + " (" +    \
+                                       __FILE__ + ":" + std::to_string(__LINE__) + ")");       \
+    } while (0)
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return FPG_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return FPG_ENOMEM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return FPG_ECUDA;
+    }
+}
+
+inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+inline int stride_of(int len) { return len <= 16 ? 16 : (len + 15) & ~15; }
+
+// Device buffer that grows on demand (never shrinks), freed on destruction.
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t cap = 0;  // elements
+    int dev = -1;
+    void reserve(size_t n) {
+        if (n <= cap && p) return;
+        release();
+        size_t want = std::max<size_t>(n, 1);
+        CK(cudaMalloc(&p, want * sizeof(T)));
+        cap = want;
+        CK(cudaGetDevice(&dev));
+    }
+    void release() {
+        if (p) {
+            int cur = -1;
+            cudaGetDevice(&cur);
+            if (dev >= 0 && cur != dev) cudaSetDevice(dev);
+            cudaFree(p);
+            if (dev >= 0 && cur != dev) cudaSetDevice(cur);
+        }
+        p = nullptr;
+        cap = 0;
+    }
+    ~DBuf() { release(); }
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+};
+
+// Pinned host buffer.
+template <class T>
+struct HBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    void reserve(size_t n) {
+        if (n <= cap && p) return;
+        release();
+        size_t want = std::max<size_t>(n, 1);
+        CK(cudaMallocHost(&p, want * sizeof(T)));
+        cap = want;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+    ~HBuf() { release(); }
+    HBuf() = default;
+    HBuf(const HBuf&) = delete;
+    HBuf& operator=(const HBuf&) = delete;
+};
+
+fpg::SchemeParams make_params(const fpg_scheme& s) {
+    fpg::SchemeParams P;
+    std::memset(&P, 0, sizeof(P));
+    for (int c = 0; c < 256; ++c) P.slot[c] = -1;
+    for (int i = 0; i < s.nletters; ++i) P.slot[s.letters[i]] = (int8_t)i;
+    P.variant = s.variant;
+    P.width = s.width;
+    P.b = s.bits_per_count;
+    P.p = s.bits_per_position;
+    P.nletters = s.nletters;
+    const int W = s.width;
+    P.full = W == 64 ? ~0ull : ((1ull << W) - 1);
+    if (s.variant == FPG_COUNT) {
+        for (int q = 0; q < W / P.b; ++q) P.mask_fold |= 1ull << (W - P.b * (q + 1));
+    } else if (s.variant == FPG_POSITION) {
+        P.slots = W / P.p;
+        P.extra = W - P.slots * P.p;
+        for (int q = 0; q < P.slots; ++q) P.mask_fold |= 1ull << (W - P.p * (q + 1));
+        for (int q = 0; q < P.extra; ++q) P.mask_single |= 1ull << q;
+    }
+    return P;
+}
+
+int capacity(int32_t variant, int32_t width, int32_t b, int32_t p) {
+    if (width != 16 && width != 32 && width != 64) return FPG_EINVAL;
+    switch (variant) {
+        case FPG_OCCURRENCE: return width;
+        case FPG_OCCURRENCE_HALVED: return width / 2;
+        case FPG_COUNT: return (b <= 0 || width % b) ? FPG_EINVAL : width / b;
+        case FPG_POSITION: {
+            if (p <= 0 || p > width) return FPG_EINVAL;
+            const int slots = width / p;
+            return slots + (width - slots * p);
+        }
+    }
+    return FPG_EINVAL;
+}
+
+void validate(const fpg_scheme* s) {
+    if (!s) throw Error(FPG_EINVAL, "null scheme");
+    const int cap = capacity(s->variant, s->width, s->bits_per_count, s->bits_per_position);
+    if (cap < 0) throw Error(FPG_EINVAL, "invalid scheme parameters (variant/width/b/p)");
+    if (s->nletters != cap)
+        throw Error(FPG_EINVAL, "scheme requires " + std::to_string(cap) + " letters, got " +
+                                    std::to_string(s->nletters));
+    bool seen[256] = {false};
+    for (int i = 0; i < s->nletters; ++i) {
+        if (seen[s->letters[i]]) throw Error(FPG_EINVAL, "LetterSet: duplicate symbol in letter set");
+        seen[s->letters[i]] = true;
+    }
+}
+
+bool supports(int variant, int metric) {
+    return metric == FPG_HAMMING || variant == FPG_OCCURRENCE || variant == FPG_COUNT;
+}
+
+uint64_t g_launches = 0;  // approximate, per process; per-run counts are exact below
+
+// Strings of one collection, length-bucketed on one device.
+struct Collection {
+    uint64_t n = 0;
+    std::vector<uint32_t> count, start;  // per length [0, kMaxLen]
+    std::vector<uint64_t> byte_base;
+    uint64_t total_bytes = 0;
+    int max_len = 0;
+    DBuf<uint64_t> fp;
+    DBuf<uint32_t> ids;
+    DBuf<uint8_t> bytes;
+    DBuf<uint32_t> d_start;
+    DBuf<uint64_t> d_byte_base;
+    // scratch
+    DBuf<uint16_t> len_a, len_b;
+    DBuf<uint32_t> idx_a, idx_b;
+    DBuf<uint32_t> hist;
+    DBuf<uint8_t> cub_tmp;
+    HBuf<uint32_t> h_hist;
+
+    // Builds the bucketed layout of n strings already on the device.
+    // Returns the number of kernel launches issued (ours, not CUB's).
+    uint64_t build(const uint8_t* d_blob, const uint64_t* d_offs, uint64_t n_, const fpg::SchemeParams& P,
+                   cudaStream_t st) {
+        n = n_;
+        const int L1 = fpg::kMaxLen + 1;
+        count.assign(L1, 0);
+        start.assign(L1, 0);
+        byte_base.assign(L1, 0);
+        uint64_t launches = 0;
+        hist.reserve(L1 + 1);
+        h_hist.reserve(L1 + 1);
+        CK(cudaMemsetAsync(hist.p, 0, sizeof(uint32_t) * (L1 + 1), st));
+        fp.reserve(n);
+        ids.reserve(n);
+        if (n) {
+            len_a.reserve(n); len_b.reserve(n); idx_a.reserve(n); idx_b.reserve(n);
+            fpg::k_lengths<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(d_offs, n, len_a.p, idx_a.p, hist.p,
+                                                                   hist.p + L1);
+            CK(cudaGetLastError());
+            ++launches;
+        }
+        CK(cudaMemcpyAsync(h_hist.p, hist.p, sizeof(uint32_t) * (L1 + 1), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (h_hist.p[L1]) throw Error(FPG_EINVAL, "string longer than FPG_MAX_WORD_LEN");
+        uint64_t pos = 0, bytes_pos = 0;
+        max_len = 0;
+        for (int L = 0; L < L1; ++L) {
+            count[L] = h_hist.p[L];
+            start[L] = (uint32_t)pos;
+            byte_base[L] = bytes_pos;
+            pos += count[L];
+            bytes_pos += (uint64_t)count[L] * stride_of(L);
+            if (count[L]) max_len = L;
+        }
+        total_bytes = bytes_pos;
+        bytes.reserve(total_bytes);
+        d_start.reserve(L1);
+        d_byte_base.reserve(L1);
+        CK(cudaMemcpyAsync(d_start.p, start.data(), sizeof(uint32_t) * L1, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d_byte_base.p, byte_base.data(), sizeof(uint64_t) * L1, cudaMemcpyHostToDevice, st));
+        if (!n) return launches;
+        int end_bit = 1;
+        while ((1 << end_bit) <= max_len) ++end_bit;
+        size_t tmp = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, len_a.p, len_b.p, idx_a.p, idx_b.p, (int)n, 0,
+                                           end_bit, st));
+        cub_tmp.reserve(tmp);
+        CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, tmp, len_a.p, len_b.p, idx_a.p, idx_b.p, (int)n, 0,
+                                           end_bit, st));
+        const unsigned grid = (unsigned)cdiv(n, 256);
+        switch (P.variant) {
+            case 0: fpg::k_build<0><<<grid, 256, 0, st>>>(d_blob, d_offs, idx_b.p, n, d_start.p, d_byte_base.p, P, fp.p, ids.p, bytes.p); break;
+            case 1: fpg::k_build<1><<<grid, 256, 0, st>>>(d_blob, d_offs, idx_b.p, n, d_start.p, d_byte_base.p, P, fp.p, ids.p, bytes.p); break;
+            case 2: fpg::k_build<2><<<grid, 256, 0, st>>>(d_blob, d_offs, idx_b.p, n, d_start.p, d_byte_base.p, P, fp.p, ids.p, bytes.p); break;
+            default: fpg::k_build<3><<<grid, 256, 0, st>>>(d_blob, d_offs, idx_b.p, n, d_start.p, d_byte_base.p, P, fp.p, ids.p, bytes.p); break;
+        }
+        CK(cudaGetLastError());
+        return launches + 1;
+    }
+
+    void drop_scratch() {
+        len_a.release(); len_b.release(); idx_a.release(); idx_b.release(); cub_tmp.release();
+    }
+};
+
+struct Shard {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint64_t base = 0, n = 0;  // input index range [base, base + n)
+    Collection dict;
+};
+
+}  // namespace
+
+struct fpg_dict {
+    fpg_scheme scheme;
+    fpg::SchemeParams params;
+    uint64_t n = 0, id_base = 0;
+    std::vector<std::unique_ptr<Shard>> shards;
+    std::vector<uint64_t> len_count;  // whole-dictionary bucket counts (all shards)
+    double build_seconds = 0;
+    std::mutex cache_mu;              // guards `cached` (fpg_query_batch reuses its scratch)
+    fpg_batch* cached = nullptr;
+    ~fpg_dict();
+};
+
+namespace {
+
+struct ShardBatch {
+    Shard* sh = nullptr;
+    DBuf<uint8_t> qblob;
+    DBuf<uint64_t> qoffs;
+    Collection queries;
+    DBuf<fpg::Tile> tiles;
+    DBuf<unsigned long long> out, sorted;
+    DBuf<unsigned long long> counters;  // [0] out_count, [1] survivors_total
+    DBuf<uint32_t> qsurv;
+    DBuf<uint64_t> offsets;
+    DBuf<uint32_t> ids;
+    DBuf<uint8_t> cub_tmp;
+    HBuf<unsigned long long> h_counters;
+    HBuf<uint64_t> h_offsets;
+    HBuf<uint32_t> h_ids, h_qsurv;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    uint64_t total = 0, executed = 0, survivors = 0, launches = 0;
+    double run_ms = 0, filter_ms = 0;
+    uint64_t out_cap = 1 << 20;
+};
+
+}  // namespace
+
+struct fpg_batch {
+    fpg_dict* dict = nullptr;
+    uint64_t nq = 0;
+    std::vector<uint32_t> qlen;  // host copy of query lengths (stats bookkeeping)
+    std::vector<std::unique_ptr<ShardBatch>> sb;
+    fpg_query_options opt{};
+    bool ran = false;
+    ~fpg_batch() {
+        for (auto& s : sb) {
+            cudaSetDevice(s->sh->device);
+            for (auto e : s->ev)
+                if (e) cudaEventDestroy(e);
+        }
+    }
+};
+
+fpg_dict::~fpg_dict() {
+    delete cached;
+    for (auto& s : shards) {
+        cudaSetDevice(s->device);
+        if (s->stream) cudaStreamDestroy(s->stream);
+    }
+}
+
+namespace {
+
+template <class F>
+void for_each_shard(size_t n, F&& f) {
+    if (n == 1) {
+        f(0);
+        return;
+    }
+    std::vector<std::thread> th;
+    std::vector<std::string> errs(n);
+    std::vector<int> codes(n, 0);
+    for (size_t i = 0; i < n; ++i)
+        th.emplace_back([&, i] {
+            try {
+                f(i);
+            } catch (const Error& e) {
+                errs[i] = e.what();
+                codes[i] = e.code;
+            } catch (const std::exception& e) {
+                errs[i] = e.what();
+                codes[i] = FPG_ECUDA;
+            }
+        });
+    for (auto& t : th) t.join();
+    for (size_t i = 0; i < n; ++i)
+        if (codes[i]) throw Error(codes[i], "shard " + std::to_string(i) + ": " + errs[i]);
+}
+
+template <int VARIANT, int W>
+void launch_scan(const fpg::Tile* tiles, uint32_t ntiles, const fpg::ScanParams& P, int fold,
+                 cudaStream_t st, int device) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fpg::k_scan<VARIANT, W>, fpg::kScanThreads, 0));
+    const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)sms * std::max(per_sm, 1) * 4);
+    fpg::k_scan<VARIANT, W><<<(unsigned)std::max<uint64_t>(grid, 1), fpg::kScanThreads, 0, st>>>(tiles, ntiles, P, fold);
+    CK(cudaGetLastError());
+}
+
+void dispatch_scan(int variant, int width, const fpg::Tile* tiles, uint32_t ntiles, const fpg::ScanParams& P,
+                   int fold, cudaStream_t st, int device) {
+#define FPG_W(V)                                                                           \
+    if (width == 16) launch_scan<V, 16>(tiles, ntiles, P, fold, st, device);               \
+    else if (width == 32) launch_scan<V, 32>(tiles, ntiles, P, fold, st, device);          \
+    else launch_scan<V, 64>(tiles, ntiles, P, fold, st, device);
+    switch (variant) {
+        case 0: FPG_W(0) break;
+        case 1: FPG_W(1) break;
+        case 2: FPG_W(2) break;
+        default: FPG_W(3) break;
+    }
+#undef FPG_W
+}
+
+bool compatible(int metric, int k, int lq, int lw) {
+    if (metric == FPG_HAMMING) return lq == lw;
+    return std::abs(lq - lw) <= k;
+}
+
+// Plans tiles, scans, orders matches into a CSR on the shard's device.
+void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options& o) {
+    Shard& sh = *S.sh;
+    CK(cudaSetDevice(sh.device));
+    cudaStream_t st = sh.stream;
+    for (auto& e : S.ev)
+        if (!e) CK(cudaEventCreate(&e));
+    S.launches = 0;
+    CK(cudaEventRecord(S.ev[0], st));
+    const uint64_t nq = B->nq;
+    // K1 on the queries (pattern fingerprint inside query time, dictionary.hpp:84)
+    S.launches += S.queries.build(S.qblob.p, S.qoffs.p, nq, D->params, st);
+    const Collection& Q = S.queries;
+    const Collection& W = sh.dict;
+
+    // Tile plan over compatible (query length, word length) bucket pairs.
+    const bool count_only_pass = o.want_stats && o.use_filter && o.metric == FPG_LEVENSHTEIN && !o.length_prefilter;
+    std::vector<fpg::Tile> plan;
+    uint64_t executed = 0;
+    for (int lq = 0; lq <= Q.max_len; ++lq) {
+        if (!Q.count[lq]) continue;
+        for (int lw = 0; lw <= W.max_len; ++lw) {
+            if (!W.count[lw]) continue;
+            const bool comp = compatible(o.metric, o.k, lq, lw);
+            if (!comp && !count_only_pass) continue;
+            if (comp) executed += (uint64_t)Q.count[lq] * W.count[lw];
+            for (uint32_t q0 = 0; q0 < Q.count[lq]; q0 += fpg::kTileQueries) {
+                for (uint32_t w0 = 0; w0 < W.count[lw]; w0 += fpg::kTileWords) {
+                    fpg::Tile t{};
+                    t.q_begin = Q.start[lq] + q0;
+                    t.q_count = std::min<uint32_t>(fpg::kTileQueries, Q.count[lq] - q0);
+                    t.w_begin = W.start[lw] + w0;
+                    t.w_count = std::min<uint32_t>(fpg::kTileWords, W.count[lw] - w0);
+                    t.q_bytes = Q.byte_base[lq] + (uint64_t)q0 * stride_of(lq);
+                    t.w_bytes = W.byte_base[lw] + (uint64_t)w0 * stride_of(lw);
+                    t.q_len = (uint16_t)lq;
+                    t.w_len = (uint16_t)lw;
+                    t.q_stride = (uint16_t)stride_of(lq);
+                    t.w_stride = (uint16_t)stride_of(lw);
+                    t.count_only = comp ? 0u : 1u;
+                    plan.push_back(t);
+                }
+            }
+        }
+    }
+    S.executed = executed;
+    S.tiles.reserve(plan.size());
+    if (!plan.empty())
+        CK(cudaMemcpyAsync(S.tiles.p, plan.data(), plan.size() * sizeof(fpg::Tile), cudaMemcpyHostToDevice, st));
+
+    S.qsurv.reserve(nq);
+    S.counters.reserve(2);
+    S.h_counters.reserve(2);
+    fpg::ScanParams P{};
+    P.q_fp = Q.fp.p;
+    P.q_bytes = Q.bytes.p;
+    P.q_ids = Q.ids.p;
+    P.w_fp = W.fp.p;
+    P.w_bytes = W.bytes.p;
+    P.w_ids = W.ids.p;
+    P.id_base = D->id_base + sh.base;
+    P.q_survivors = S.qsurv.p;
+    P.out_count = S.counters.p;
+    P.survivors_total = S.counters.p + 1;
+    P.mask_fold = D->params.mask_fold;
+    P.mask_single = D->params.mask_single;
+    P.thr = o.use_filter ? 2 * o.k : 1 << 20;
+    P.k = o.k;
+    const int fold = D->params.variant == FPG_COUNT ? D->params.b
+                   : D->params.variant == FPG_POSITION ? D->params.p : 1;
+    for (;;) {
+        S.out.reserve(S.out_cap);
+        P.out = S.out.p;
+        P.out_cap = S.out.cap;
+        CK(cudaMemsetAsync(S.counters.p, 0, 2 * sizeof(unsigned long long), st));
+        if (nq) CK(cudaMemsetAsync(S.qsurv.p, 0, nq * sizeof(uint32_t), st));
+        CK(cudaEventRecord(S.ev[1], st));
+        if (!plan.empty()) {
+            dispatch_scan(D->params.variant, D->params.width, S.tiles.p, (uint32_t)plan.size(), P, fold, st, sh.device);
+            ++S.launches;
+        }
+        CK(cudaEventRecord(S.ev[2], st));
+        CK(cudaMemcpyAsync(S.h_counters.p, S.counters.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (S.h_counters.p[0] <= S.out.cap) break;
+        S.out_cap = S.h_counters.p[0] + S.h_counters.p[0] / 4 + 1024;  // grow and rescan
+    }
+    S.total = S.h_counters.p[0];
+    S.survivors = S.h_counters.p[1];
+
+    // K4: order (query, word) keys and build the CSR.
+    S.sorted.reserve(S.total);
+    S.offsets.reserve(nq + 1);
+    S.ids.reserve(S.total);
+    if (S.total) {
+        int end_bit = 33;
+        while (end_bit < 64 && (1ull << (end_bit - 32)) <= nq) ++end_bit;
+        size_t tmp = 0;
+        CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, S.out.p, S.sorted.p, (int)S.total, 0, end_bit, st));
+        S.cub_tmp.reserve(tmp);
+        CK(cub::DeviceRadixSort::SortKeys(S.cub_tmp.p, tmp, S.out.p, S.sorted.p, (int)S.total, 0, end_bit, st));
+        fpg::k_low_ids<<<(unsigned)cdiv(S.total, 256), 256, 0, st>>>(S.sorted.p, S.total, S.ids.p);
+        CK(cudaGetLastError());
+        ++S.launches;
+    }
+    fpg::k_offsets<<<(unsigned)cdiv(nq + 1, 256), 256, 0, st>>>(S.sorted.p, S.total, nq, S.offsets.p);
+    CK(cudaGetLastError());
+    ++S.launches;
+    CK(cudaEventRecord(S.ev[3], st));
+    CK(cudaEventSynchronize(S.ev[3]));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, S.ev[0], S.ev[3]));
+    S.run_ms = ms;
+    CK(cudaEventElapsedTime(&ms, S.ev[1], S.ev[2]));
+    S.filter_ms = ms;
+    g_launches += S.launches;
+}
+
+void download_shard(fpg_batch* B, ShardBatch& S, bool stats) {
+    CK(cudaSetDevice(S.sh->device));
+    cudaStream_t st = S.sh->stream;
+    const uint64_t nq = B->nq;
+    S.h_offsets.reserve(nq + 1);
+    S.h_ids.reserve(S.total);
+    CK(cudaMemcpyAsync(S.h_offsets.p, S.offsets.p, (nq + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    if (S.total) CK(cudaMemcpyAsync(S.h_ids.p, S.ids.p, S.total * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    if (stats && nq) {
+        S.h_qsurv.reserve(nq);
+        CK(cudaMemcpyAsync(S.h_qsurv.p, S.qsurv.p, nq * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+}
+
+void check_opts(const fpg_dict* D, const fpg_query_options* o) {
+    if (!o) throw Error(FPG_EINVAL, "null options");
+    if (o->metric != FPG_HAMMING && o->metric != FPG_LEVENSHTEIN) throw Error(FPG_EINVAL, "unknown metric");
+    if (o->use_filter && !supports(D->scheme.variant, o->metric))
+        throw Error(FPG_EINVAL, "scheme does not filter for this metric");
+    if (o->k < 0 || o->k > 1)
+        throw Error(FPG_EUNSUPPORTED, "GPU scan supports k in {0, 1}, got " + std::to_string(o->k));
+}
+
+void upload(fpg_batch* B, const uint8_t* qbytes, const uint64_t* qoffsets, uint64_t nq) {
+    if (nq && !qoffsets) throw Error(FPG_EINVAL, "null query offsets");
+    if (nq >= (1ull << 31)) throw Error(FPG_EINVAL, "too many queries in one batch");
+    B->nq = nq;
+    B->qlen.resize(nq);
+    const uint64_t q0 = nq ? qoffsets[0] : 0;
+    for (uint64_t i = 0; i < nq; ++i) {
+        if (qoffsets[i + 1] < qoffsets[i]) throw Error(FPG_EINVAL, "query offsets not ascending");
+        const uint64_t len = qoffsets[i + 1] - qoffsets[i];
+        if (len > (uint64_t)fpg::kMaxLen) throw Error(FPG_EINVAL, "query longer than FPG_MAX_WORD_LEN");
+        B->qlen[i] = (uint32_t)len;
+    }
+    const uint64_t nbytes = nq ? qoffsets[nq] - q0 : 0;
+    for_each_shard(B->sb.size(), [&](size_t i) {
+        ShardBatch& S = *B->sb[i];
+        CK(cudaSetDevice(S.sh->device));
+        S.qblob.reserve(nbytes);
+        S.qoffs.reserve(nq + 1);
+        if (nbytes) CK(cudaMemcpyAsync(S.qblob.p, qbytes + q0, nbytes, cudaMemcpyHostToDevice, S.sh->stream));
+        if (nq) {
+            if (q0 == 0) {
+                CK(cudaMemcpyAsync(S.qoffs.p, qoffsets, (nq + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, S.sh->stream));
+            } else {
+                std::vector<uint64_t> rebased(nq + 1);
+                for (uint64_t j = 0; j <= nq; ++j) rebased[j] = qoffsets[j] - q0;
+                CK(cudaMemcpyAsync(S.qoffs.p, rebased.data(), (nq + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, S.sh->stream));
+                CK(cudaStreamSynchronize(S.sh->stream));
+            }
+        }
+    });
+}
+
+void run(fpg_batch* B, const fpg_query_options* o) {
+    check_opts(B->dict, o);
+    B->opt = *o;
+    for_each_shard(B->sb.size(), [&](size_t i) { run_shard(B->dict, B, *B->sb[i], *o); });
+    B->ran = true;
+}
+
+// Assembles the caller-visible CSR (+ QueryStats) from the shards.
+void download(fpg_batch* B, fpg_result* out) {
+    if (!B->ran) throw Error(FPG_EINVAL, "fpg_batch_download before fpg_batch_run");
+    const fpg_query_options& o = B->opt;
+    const bool stats = o.want_stats != 0;
+    for_each_shard(B->sb.size(), [&](size_t i) { download_shard(B, *B->sb[i], stats); });
+    const uint64_t nq = B->nq;
+    std::memset(out, 0, sizeof(*out));
+    out->nq = nq;
+    uint64_t total = 0;
+    for (auto& s : B->sb) total += s->total;
+    out->total = total;
+    out->offsets = static_cast<uint64_t*>(std::malloc(sizeof(uint64_t) * (nq + 1)));
+    out->word_ids = static_cast<uint32_t*>(std::malloc(sizeof(uint32_t) * std::max<uint64_t>(total, 1)));
+    if (!out->offsets || !out->word_ids) throw std::bad_alloc();
+    if (B->sb.size() == 1) {
+        ShardBatch& S = *B->sb[0];
+        std::memcpy(out->offsets, S.h_offsets.p, sizeof(uint64_t) * (nq + 1));
+        if (total) std::memcpy(out->word_ids, S.h_ids.p, sizeof(uint32_t) * total);
+    } else {
+        // Shards own ascending contiguous id ranges: concatenating each query's
+        // shard rows in shard order yields ascending ids (oracle order).
+        uint64_t pos = 0;
+        for (uint64_t q = 0; q < nq; ++q) {
+            out->offsets[q] = pos;
+            for (auto& s : B->sb) {
+                const uint64_t a = s->h_offsets.p[q], b = s->h_offsets.p[q + 1];
+                if (b > a) std::memcpy(out->word_ids + pos, s->h_ids.p + a, sizeof(uint32_t) * (b - a));
+                pos += b - a;
+            }
+        }
+        out->offsets[nq] = pos;
+    }
+    if (stats) {
+        out->stats = static_cast<uint64_t*>(std::calloc(FPG_NSTATS * std::max<uint64_t>(nq, 1), sizeof(uint64_t)));
+        if (!out->stats) throw std::bad_alloc();
+        const fpg_dict* D = B->dict;
+        const uint64_t N = D->n;
+        // prefix sums of bucket counts for compatible-range queries
+        const int L1 = fpg::kMaxLen + 1;
+        for (uint64_t q = 0; q < nq; ++q) {
+            const int lq = (int)B->qlen[q];
+            uint64_t surv = 0;
+            for (auto& s : B->sb) surv += s->h_qsurv.p[q];
+            uint64_t comp = 0;
+            const bool all = o.metric == FPG_LEVENSHTEIN && !o.length_prefilter;
+            if (all) {
+                comp = N;
+            } else {
+                const int lo = o.metric == FPG_HAMMING ? lq : std::max(0, lq - o.k);
+                const int hi = o.metric == FPG_HAMMING ? lq : std::min(L1 - 1, lq + o.k);
+                for (int L = lo; L <= hi; ++L) comp += D->len_count[L];
+            }
+            uint64_t* st = out->stats + FPG_NSTATS * q;
+            st[FPG_STAT_COMPARED] = N;
+            st[FPG_STAT_REJECTED_BY_LENGTH] = N - comp;
+            const uint64_t verified = o.use_filter ? surv : comp;
+            st[FPG_STAT_VERIFIED] = verified;
+            st[FPG_STAT_REJECTED_BY_FINGERPRINT] = comp - verified;
+            st[FPG_STAT_MATCHES] = out->offsets[q + 1] - out->offsets[q];
+        }
+    }
+}
+
+void make_batch(fpg_dict* D, fpg_batch** out) {
+    auto B = std::make_unique<fpg_batch>();
+    B->dict = D;
+    for (auto& sh : D->shards) {
+        auto S = std::make_unique<ShardBatch>();
+        S->sh = sh.get();
+        B->sb.push_back(std::move(S));
+    }
+    *out = B.release();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fpg_last_error(void) { return g_last_error.c_str(); }
+int fpg_abi_version(void) { return FPG_ABI_VERSION; }
+
+int fpg_device_count(int* count) {
+    return guarded([&] {
+        int n = 0;
+        CK(cudaGetDeviceCount(&n));
+        *count = n;
+    });
+}
+
+int fpg_letter_capacity(int32_t variant, int32_t width, int32_t b, int32_t p) {
+    const int c = capacity(variant, width, b, p);
+    if (c < 0) g_last_error = "invalid scheme parameters";
+    return c;
+}
+
+int fpg_scheme_validate(const fpg_scheme* scheme) {
+    return guarded([&] { validate(scheme); });
+}
+
+int fpg_scheme_supports(const fpg_scheme* scheme, int32_t metric) {
+    return scheme && supports(scheme->variant, metric) ? 1 : 0;
+}
+
+int fpg_dict_create(const uint8_t* bytes, const uint64_t* offsets, uint64_t n, const fpg_scheme* scheme,
+                    const int32_t* devices, int32_t ndevices, uint64_t id_base, fpg_dict** out) {
+    return guarded([&] {
+        validate(scheme);
+        if (!out) throw Error(FPG_EINVAL, "null output handle");
+        if (n && (!offsets || !bytes)) throw Error(FPG_EINVAL, "null dictionary buffers");
+        if (n >= (1ull << 32) - 1) throw Error(FPG_EINVAL, "dictionary too large for 32-bit ids");
+        if (id_base + n > (1ull << 32)) throw Error(FPG_EINVAL, "id_base + n exceeds 32-bit ids");
+        std::vector<int32_t> devs;
+        if (devices && ndevices > 0) devs.assign(devices, devices + ndevices);
+        else devs.push_back(0);
+        int ndev = 0;
+        CK(cudaGetDeviceCount(&ndev));
+        for (int d : devs)
+            if (d < 0 || d >= ndev) throw Error(FPG_EINVAL, "device " + std::to_string(d) + " not present");
+        auto t0 = std::chrono::steady_clock::now();
+        auto D = std::make_unique<fpg_dict>();
+        D->scheme = *scheme;
+        D->params = make_params(*scheme);
+        D->n = n;
+        D->id_base = id_base;
+        D->len_count.assign(fpg::kMaxLen + 1, 0);
+        const size_t G = devs.size();
+        for (size_t g = 0; g < G; ++g) {
+            auto sh = std::make_unique<Shard>();
+            sh->device = devs[g];
+            sh->base = n * g / G;
+            sh->n = n * (g + 1) / G - sh->base;
+            D->shards.push_back(std::move(sh));
+        }
+        for_each_shard(G, [&](size_t g) {
+            Shard& sh = *D->shards[g];
+            CK(cudaSetDevice(sh.device));
+            CK(cudaStreamCreateWithFlags(&sh.stream, cudaStreamNonBlocking));
+            const uint64_t b0 = sh.n ? offsets[sh.base] : 0;
+            const uint64_t nbytes = sh.n ? offsets[sh.base + sh.n] - b0 : 0;
+            DBuf<uint8_t> blob;
+            DBuf<uint64_t> offs;
+            blob.reserve(nbytes);
+            offs.reserve(sh.n + 1);
+            std::vector<uint64_t> local(sh.n + 1);
+            for (uint64_t i = 0; i <= sh.n; ++i) local[i] = (sh.n ? offsets[sh.base + i] : 0) - b0;
+            if (nbytes) CK(cudaMemcpyAsync(blob.p, bytes + b0, nbytes, cudaMemcpyHostToDevice, sh.stream));
+            CK(cudaMemcpyAsync(offs.p, local.data(), (sh.n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, sh.stream));
+            sh.dict.build(blob.p, offs.p, sh.n, D->params, sh.stream);
+            CK(cudaStreamSynchronize(sh.stream));
+            sh.dict.drop_scratch();
+        });
+        for (auto& sh : D->shards)
+            for (int L = 0; L <= fpg::kMaxLen; ++L) D->len_count[L] += sh->dict.count[L];
+        D->build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        *out = D.release();
+    });
+}
+
+int fpg_dict_destroy(fpg_dict* dict) {
+    return guarded([&] { delete dict; });
+}
+
+int fpg_dict_size(const fpg_dict* dict, uint64_t* n) {
+    return guarded([&] {
+        if (!dict || !n) throw Error(FPG_EINVAL, "null argument");
+        *n = dict->n;
+    });
+}
+
+int fpg_dict_build_seconds(const fpg_dict* dict, double* seconds) {
+    return guarded([&] {
+        if (!dict || !seconds) throw Error(FPG_EINVAL, "null argument");
+        *seconds = dict->build_seconds;
+    });
+}
+
+int fpg_dict_prints(const fpg_dict* dict, uint64_t* out) {
+    return guarded([&] {
+        if (!dict || (!out && dict->n)) throw Error(FPG_EINVAL, "null argument");
+        for (auto& shp : dict->shards) {
+            Shard& sh = *shp;
+            if (!sh.n) continue;
+            CK(cudaSetDevice(sh.device));
+            DBuf<uint64_t> tmp;
+            tmp.reserve(sh.n);
+            fpg::k_scatter_prints<<<(unsigned)cdiv(sh.n, 256), 256, 0, sh.stream>>>(sh.dict.fp.p, sh.dict.ids.p, sh.n, tmp.p);
+            CK(cudaGetLastError());
+            CK(cudaMemcpyAsync(out + sh.base, tmp.p, sh.n * sizeof(uint64_t), cudaMemcpyDeviceToHost, sh.stream));
+            CK(cudaStreamSynchronize(sh.stream));
+        }
+    });
+}
+
+int fpg_build_fingerprints(const uint8_t* bytes, const uint64_t* offsets, uint64_t n, const fpg_scheme* scheme,
+                           int32_t device, uint64_t* out) {
+    return guarded([&] {
+        validate(scheme);
+        if (n && (!bytes || !offsets || !out)) throw Error(FPG_EINVAL, "null argument");
+        CK(cudaSetDevice(device));
+        if (!n) return;
+        const fpg::SchemeParams P = make_params(*scheme);
+        const uint64_t b0 = offsets[0], nbytes = offsets[n] - b0;
+        std::vector<uint64_t> local(n + 1);
+        for (uint64_t i = 0; i <= n; ++i) {
+            local[i] = offsets[i] - b0;
+            if (i && offsets[i] - offsets[i - 1] > (uint64_t)fpg::kMaxLen)
+                throw Error(FPG_EINVAL, "string longer than FPG_MAX_WORD_LEN");
+        }
+        cudaStream_t st;
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        std::unique_ptr<CUstream_st, void (*)(CUstream_st*)> guard(st, [](CUstream_st* s) { cudaStreamDestroy(s); });
+        DBuf<uint8_t> blob;
+        DBuf<uint64_t> offs, fp;
+        blob.reserve(nbytes);
+        offs.reserve(n + 1);
+        fp.reserve(n);
+        if (nbytes) CK(cudaMemcpyAsync(blob.p, bytes + b0, nbytes, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(offs.p, local.data(), (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+        const unsigned grid = (unsigned)cdiv(n, 256);
+        switch (P.variant) {
+            case 0: fpg::k_build<0><<<grid, 256, 0, st>>>(blob.p, offs.p, nullptr, n, nullptr, nullptr, P, fp.p, nullptr, nullptr); break;
+            case 1: fpg::k_build<1><<<grid, 256, 0, st>>>(blob.p, offs.p, nullptr, n, nullptr, nullptr, P, fp.p, nullptr, nullptr); break;
+            case 2: fpg::k_build<2><<<grid, 256, 0, st>>>(blob.p, offs.p, nullptr, n, nullptr, nullptr, P, fp.p, nullptr, nullptr); break;
+            default: fpg::k_build<3><<<grid, 256, 0, st>>>(blob.p, offs.p, nullptr, n, nullptr, nullptr, P, fp.p, nullptr, nullptr); break;
+        }
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(out, fp.p, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    });
+}
+
+int fpg_batch_create(fpg_dict* dict, fpg_batch** out) {
+    return guarded([&] {
+        if (!dict || !out) throw Error(FPG_EINVAL, "null argument");
+        make_batch(dict, out);
+    });
+}
+
+int fpg_batch_destroy(fpg_batch* batch) {
+    return guarded([&] { delete batch; });
+}
+
+int fpg_batch_upload(fpg_batch* batch, const uint8_t* qbytes, const uint64_t* qoffsets, uint64_t nq) {
+    return guarded([&] {
+        if (!batch) throw Error(FPG_EINVAL, "null batch");
+        upload(batch, qbytes, qoffsets, nq);
+        batch->ran = false;
+    });
+}
+
+int fpg_batch_run(fpg_batch* batch, const fpg_query_options* opt) {
+    return guarded([&] {
+        if (!batch) throw Error(FPG_EINVAL, "null batch");
+        run(batch, opt);
+    });
+}
+
+int fpg_batch_download(fpg_batch* batch, fpg_result* out) {
+    return guarded([&] {
+        if (!batch || !out) throw Error(FPG_EINVAL, "null argument");
+        download(batch, out);
+    });
+}
+
+int fpg_batch_last_timing(const fpg_batch* batch, int32_t shard, double* run_ms, double* filter_ms,
+                          uint64_t* executed_pairs, uint64_t* survivors, uint64_t* kernel_launches) {
+    return guarded([&] {
+        if (!batch || shard < 0 || (size_t)shard >= batch->sb.size()) throw Error(FPG_EINVAL, "bad shard");
+        const ShardBatch& S = *batch->sb[(size_t)shard];
+        if (run_ms) *run_ms = S.run_ms;
+        if (filter_ms) *filter_ms = S.filter_ms;
+        if (executed_pairs) *executed_pairs = S.executed;
+        if (survivors) *survivors = S.survivors;
+        if (kernel_launches) *kernel_launches = S.launches;
+    });
+}
+
+int fpg_query_batch(fpg_dict* dict, const uint8_t* qbytes, const uint64_t* qoffsets, uint64_t nq,
+                    const fpg_query_options* opt, fpg_result* out) {
+    return guarded([&] {
+        if (!dict || !out) throw Error(FPG_EINVAL, "null argument");
+        check_opts(dict, opt);
+        // Reuse the dictionary's cached scratch when no other thread holds it.
+        std::unique_lock<std::mutex> lk(dict->cache_mu, std::try_to_lock);
+        std::unique_ptr<fpg_batch> temp;
+        fpg_batch* b = nullptr;
+        if (lk.owns_lock()) {
+            if (!dict->cached) make_batch(dict, &dict->cached);
+            b = dict->cached;
+        } else {
+            make_batch(dict, &b);
+            temp.reset(b);
+        }
+        upload(b, qbytes, qoffsets, nq);
+        run(b, opt);
+        download(b, out);
+    });
+}
+
+int fpg_result_free(fpg_result* res) {
+    return guarded([&] {
+        if (!res) return;
+        std::free(res->offsets);
+        std::free(res->word_ids);
+        std::free(res->stats);
+        std::memset(res, 0, sizeof(*res));
+    });
+}
+
+}  // extern "C"

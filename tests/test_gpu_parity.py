@@ -1,0 +1,249 @@
+"""GPU parity: libfpg.so (through the C ABI) vs the CPU oracle on the same
+seeded inputs.  Bit-exact for fingerprints, match sets and QueryStats."""
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle.oracle import oscheme, pack
+from paper_1711_08475_b200 import (GpuFingerprintedDictionary, LetterSet, Metric, QueryOptions,
+                                   QueryStats, Scheme, Variant, build, build_many, render)
+from paper_1711_08475_b200.corpus import (CELLS, generate_dictionary, generate_queries, make_scheme,
+                                          subsample)
+
+pytestmark = pytest.mark.gpu
+GOLD = json.loads((Path(__file__).parent / "golden" / "reference_vectors.json").read_text())
+
+
+def osch(s: Scheme):
+    return oscheme(int(s.variant()), s.letters().symbols(), s.width(), s.bits_per_count() or 2,
+                   s.bits_per_position() or 3)
+
+
+def fixture_scheme(rec, width=16):
+    return Scheme.make(Variant(rec["variant"]), LetterSet(rec["letters"]), rec["b"], rec["p"], width)
+
+
+def assert_same(csr, st, ref_off, ref_ids, ref_st=None):
+    assert np.array_equal(csr.offsets, ref_off), "per-query match counts differ"
+    assert np.array_equal(csr.word_ids, ref_ids), "match ids differ"
+    if ref_st is not None:
+        assert np.array_equal(st, ref_st), "QueryStats differ"
+
+
+# ---------------------------------------------------------------- K1 vs the reference fixtures
+
+def test_golden_instance_renders():
+    # fingerprint_test.cpp:60-66 / acceptance_test.cpp:97-113
+    want = ["1110111000010000", "01 10 01 00 10 11 10 00", "01 01 01 00 01 10 01 00", "111 011 100 111 000 1"]
+    for rec, w in zip(GOLD["schemes"][:4], want):
+        s = fixture_scheme(rec)
+        assert render(build("instance", s), s) == w
+
+
+def test_golden_tiny_strings():
+    occ, halved, count, pos = (fixture_scheme(r) for r in GOLD["schemes"][:4])
+    assert build("", occ).bits == 0 and build("", halved).bits == 0 and build("", count).bits == 0
+    assert render(build("", pos), pos) == "111 111 111 111 111 0"          # fingerprint_test.cpp:73
+    assert render(build("e", halved), halved) == "01 00 00 00 00 00 00 00"  # :75-76
+    assert render(build("e" + "z" * 19, pos), pos) == "000 111 111 111 111 0"  # :83
+    assert render(build("zzzzzze", pos), pos) == "110 111 111 111 111 0"    # :88
+    assert build("zzzzzzze", pos) == build("zzzzzzzz", pos)                 # :85-87
+    assert render(build("eeee", count), count) == "11 00 00 00 00 00 00 00"  # :94-96
+    assert render(build("ee", count), count) == "10 00 00 00 00 00 00 00"
+
+
+@pytest.mark.parametrize("idx", range(len(GOLD["schemes"])))
+def test_prints_match_reference(idx):
+    rec = GOLD["schemes"][idx]
+    words = [bytes.fromhex(h) for h in GOLD["words"]]
+    s = fixture_scheme(rec)
+    got = build_many(words, s)
+    assert [int(x) for x in got] == rec["prints"]
+    # and through the dictionary (bucketed layout, input-order prints())
+    with GpuFingerprintedDictionary(words, s) as d:
+        assert [int(x) for x in d.prints_array()] == rec["prints"]
+
+
+@pytest.mark.parametrize("variant,width,b,p", [
+    (Variant.Occurrence, 32, 2, 3), (Variant.Occurrence, 64, 2, 3),
+    (Variant.OccurrenceHalved, 32, 2, 3), (Variant.OccurrenceHalved, 64, 2, 3),
+    (Variant.Count, 32, 2, 3), (Variant.Count, 64, 4, 3), (Variant.Count, 64, 2, 3),
+    (Variant.Position, 32, 2, 3), (Variant.Position, 64, 2, 3), (Variant.Position, 64, 2, 5),
+])
+def test_prints_wide_vs_oracle(oracle, variant, width, b, p):
+    rng = np.random.default_rng(width * 10 + int(variant))
+    alphabet = bytes(range(33, 33 + 70))
+    cap = Scheme.letter_capacity(variant, b, p, width)
+    letters = bytes(rng.permutation(np.frombuffer(alphabet, np.uint8))[:cap])
+    s = Scheme.make(variant, LetterSet(letters), b, p, width)
+    words = [bytes(rng.choice(np.frombuffer(alphabet, np.uint8), rng.integers(0, 120))) for _ in range(3000)]
+    blob, offs = pack(words)
+    assert np.array_equal(build_many((blob, offs), s), oracle.build_many(blob, offs, osch(s)))
+
+
+# ---------------------------------------------------------------- K2/K3 vs reference fixtures
+
+def _fixture_case(q):
+    rec = next(r for r in GOLD["schemes"] if r["name"] == q["scheme"])
+    return rec
+
+
+@pytest.mark.parametrize("case", range(len(GOLD["queries"])))
+def test_queries_match_reference_fixture(case):
+    q = GOLD["queries"][case]
+    s = fixture_scheme(_fixture_case(q))
+    words = [bytes.fromhex(h) for h in GOLD["query_dict"]]
+    pats = [bytes.fromhex(h) for h in GOLD["query_patterns"]]
+    opt = QueryOptions(Metric(q["metric"]), q["k"], q["use_filter"], q["length_prefilter"])
+    with GpuFingerprintedDictionary(words, s) as d:
+        csr, st = d.query_batch(pats, opt, per_query_stats=True)
+    assert_same(csr, st, np.array(q["offsets"], np.uint64), np.array(q["ids"], np.uint32),
+                np.array(q["stats"], np.uint64))
+
+
+def test_query_api_semantics():
+    """dictionary_test.cpp:64-84, :110-139, :160-170 through the mirror API."""
+    occ = Scheme.occurrence(LetterSet("etaoinshrdlcumwf"))
+    with GpuFingerprintedDictionary(["run"], occ) as d:
+        st = QueryStats()
+        assert d.query("ran", QueryOptions(Metric.Hamming, 1), st) == [0]
+        assert st.rejected_by_fingerprint == 0 and st.verified == 1
+        st0 = QueryStats()
+        assert d.query("ran", QueryOptions(Metric.Hamming, 0), st0) == []
+        assert st0.compared == st0.rejected_by_length + st0.rejected_by_fingerprint + st0.verified
+        m = [99]
+        d.query_into("run", QueryOptions(), m)
+        assert m == [0]
+    pos = Scheme.position(LetterSet("abcdef"), 3)
+    with GpuFingerprintedDictionary(["abcdef", "ghijkl"], pos) as d:
+        with pytest.raises(ValueError):
+            d.query("abcdef", QueryOptions(Metric.Levenshtein, 1, True, False))
+        assert d.query("abcdef", QueryOptions(Metric.Levenshtein, 1, False, False)) == [0]
+    with GpuFingerprintedDictionary([], occ) as d:
+        st = QueryStats()
+        assert d.query("ran", QueryOptions(), st) == [] and st.compared == 0
+
+
+# ---------------------------------------------------------------- configs vs the oracle
+
+def _cfg_inputs(cfg, n, nq):
+    blob, offs = generate_dictionary(cfg, n=n)
+    qblob, qoffs = generate_queries(cfg, blob, offs, nq=nq)
+    return blob, offs, qblob, qoffs
+
+
+@pytest.mark.parametrize("cfg,n,nq", [(1, 100_000, 1000), (2, 200_000, 600), (3, 200_000, 600), (4, 50_000, 300),
+                                      (5, 200_000, 600)])
+def test_config_cells_vs_oracle(oracle, cfg, n, nq):
+    blob, offs, qblob, qoffs = _cfg_inputs(cfg, n, nq)
+    for variant, width, b, p, metric in CELLS[cfg]:
+        s = make_scheme(blob, variant, width, b, p)
+        with GpuFingerprintedDictionary((blob, offs), s) as d:
+            assert np.array_equal(d.prints_array(), oracle.build_many(blob, offs, osch(s)))
+            for pre in ((True, False) if metric == Metric.Levenshtein else (False,)):
+                opt = QueryOptions(metric, 1, True, pre)
+                csr, st = d.query_batch((qblob, qoffs), opt, per_query_stats=True)
+                o_off, o_ids, o_st = oracle.query_batch(blob, offs, qblob, qoffs, osch(s), metric, 1, True, pre)
+                assert_same(csr, st, o_off, o_ids, o_st)
+
+
+@pytest.mark.parametrize("metric", [Metric.Hamming, Metric.Levenshtein])
+@pytest.mark.parametrize("k", [0, 1])
+def test_filter_off_and_k0(oracle, metric, k):
+    blob, offs, qblob, qoffs = _cfg_inputs(2, 50_000, 300)
+    s = make_scheme(blob, Variant.Count, 16)
+    with GpuFingerprintedDictionary((blob, offs), s) as d:
+        for use_filter in (True, False):
+            opt = QueryOptions(metric, k, use_filter, True)
+            csr, st = d.query_batch((qblob, qoffs), opt, per_query_stats=True)
+            o = oracle.query_batch(blob, offs, qblob, qoffs, osch(s), metric, k, use_filter, True)
+            assert_same(csr, st, *o)
+    naive_off, naive_ids = oracle.naive_scan_batch(blob, offs, qblob, qoffs, metric, k)
+    assert np.array_equal(csr.offsets, naive_off) and np.array_equal(csr.word_ids, naive_ids)
+
+
+def test_edge_strings(oracle):
+    """Empty strings, 1-byte strings, zero bytes, 0xff, duplicates, long strings."""
+    rng = np.random.default_rng(7)
+    words = [b"", b"", b"a", b"\x00", b"a\x00", b"\x00a", b"\xff" * 3, b"ab", b"ba"]
+    words += [bytes(rng.integers(0, 4, rng.integers(0, 40)).astype(np.uint8)) for _ in range(3000)]
+    words += [bytes(rng.integers(97, 100, 4096).astype(np.uint8)), bytes(rng.integers(97, 100, 4095).astype(np.uint8))]
+    words += words[:50]  # duplicates keep distinct ids
+    pats = [b"", b"a", b"\x00", b"\x00\x00", words[-3], words[-53][:-1] + b"\x07"]
+    pats += [bytes(rng.integers(0, 4, rng.integers(0, 40)).astype(np.uint8)) for _ in range(300)]
+    blob, offs = pack(words)
+    qblob, qoffs = pack(pats)
+    s = Scheme.occurrence(LetterSet(bytes([0, 1, 2, 3, 97, 98, 99, 255] + list(range(10, 18)))))
+    with GpuFingerprintedDictionary((blob, offs), s) as d:
+        for metric in (Metric.Hamming, Metric.Levenshtein):
+            for pre in (True, False):
+                opt = QueryOptions(metric, 1, True, pre)
+                csr, st = d.query_batch((qblob, qoffs), opt, per_query_stats=True)
+                assert_same(csr, st, *oracle.query_batch(blob, offs, qblob, qoffs, osch(s), metric, 1, True, pre))
+
+
+def test_too_long_and_invalid_args():
+    s = Scheme.occurrence(LetterSet("etaoinshrdlcumwf"))
+    with pytest.raises(ValueError):
+        GpuFingerprintedDictionary([b"a" * 4097], s)
+    with pytest.raises(ValueError):
+        Scheme.occurrence(LetterSet("abc"))
+    with pytest.raises(ValueError):
+        Scheme.count(LetterSet("etaoinsh"), 3)
+    with GpuFingerprintedDictionary(["abc"], s) as d:
+        with pytest.raises(Exception):
+            d.query("abc", QueryOptions(Metric.Hamming, 2))  # k > 1 not built for the GPU
+        csr, st = d.query_batch([], QueryOptions(), per_query_stats=True)
+        assert len(csr) == 0 and st.shape == (0, 5)
+
+
+def test_shards_equal_single_device(oracle):
+    """Dictionary sharded over [0,0,0] (three shards on one GPU, independent
+    kernels) gives the single-shard answer with rebased ids."""
+    blob, offs, qblob, qoffs = _cfg_inputs(5, 100_000, 400)
+    s = make_scheme(blob, Variant.Occurrence, 16)
+    opt = QueryOptions(Metric.Levenshtein, 1, True, False)
+    with GpuFingerprintedDictionary((blob, offs), s, devices=(0,)) as d1, \
+         GpuFingerprintedDictionary((blob, offs), s, devices=(0, 0, 0)) as d3:
+        a = d1.query_batch((qblob, qoffs), opt, per_query_stats=True)
+        b = d3.query_batch((qblob, qoffs), opt, per_query_stats=True)
+        assert np.array_equal(d1.prints_array(), d3.prints_array())
+    assert np.array_equal(a[0].offsets, b[0].offsets) and np.array_equal(a[0].word_ids, b[0].word_ids)
+    assert np.array_equal(a[1], b[1])
+
+
+def test_output_regrowth_many_matches(oracle):
+    """Config-3 short queries match tens of thousands of words each; the
+    result buffer starts at 2^20 pairs and must regrow and rescan."""
+    blob, offs = generate_dictionary(3, n=400_000)
+    words = [b"e", b"t", b"ea", b"te", b"th", b"an", b"a"] * 40
+    qblob, qoffs = pack(words)
+    s = make_scheme(blob, Variant.Occurrence, 16)
+    with GpuFingerprintedDictionary((blob, offs), s) as d:
+        csr, st = d.query_batch((qblob, qoffs), QueryOptions(Metric.Levenshtein, 1, True, True), True)
+    assert csr.offsets[-1] > (1 << 20)
+    assert_same(csr, st, *oracle.query_batch(blob, offs, qblob, qoffs, osch(s), Metric.Levenshtein, 1, True, True))
+
+
+@pytest.mark.slow
+def test_config2_full_dictionary_subsample(oracle):
+    """Full config 2 (1e6 words, 10,000 queries) on the GPU; every 10th query
+    checked against the oracle, and the batch is self-consistent:
+    filter on == filter off, 1 shard == 2 shards."""
+    blob, offs, qblob, qoffs = _cfg_inputs(2, None, None)
+    s = make_scheme(blob, Variant.Count, 16)
+    opt = QueryOptions(Metric.Levenshtein, 1, True, True)
+    with GpuFingerprintedDictionary((blob, offs), s) as d:
+        csr, st = d.query_batch((qblob, qoffs), opt, per_query_stats=True)
+        off_nf, _ = d.query_batch((qblob, qoffs), QueryOptions(Metric.Levenshtein, 1, False, True))
+    sb, so, idx = subsample(qblob, qoffs, 10)
+    o_off, o_ids, o_st = oracle.query_batch(blob, offs, sb, so, osch(s), Metric.Levenshtein, 1, True, True)
+    for j, q in enumerate(idx):
+        assert np.array_equal(csr.row(q), o_ids[int(o_off[j]):int(o_off[j + 1])])
+        assert np.array_equal(st[q], o_st[j])
+    assert np.array_equal(csr.offsets, off_nf.offsets) and np.array_equal(csr.word_ids, off_nf.word_ids)
+    with GpuFingerprintedDictionary((blob, offs), s, devices=(0, 0)) as d2:
+        c2, _ = d2.query_batch((qblob, qoffs), opt)
+    assert np.array_equal(csr.word_ids, c2.word_ids)
