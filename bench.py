@@ -123,16 +123,17 @@ def workload(cfg: int, cell: int, rank: int, world: int):
     return c, blob, offs, qblob, qoffs, scheme, metric, first, n
 
 
+_PINNED = []  # owners of pinned host storage
+
+
 def pinned_copy(a: np.ndarray) -> np.ndarray:
+    """Copy of `a` in page-locked host memory (torch pinned allocator)."""
     import torch
 
-    t = torch.empty(a.size, dtype=torch.uint8, pin_memory=True)
-    v = t.numpy().view(a.dtype)[: a.size] if a.dtype == np.uint8 else None
-    if v is None:
-        t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
-        v = t.numpy().view(a.dtype)
+    t = torch.empty(max(a.nbytes, 1), dtype=torch.uint8, pin_memory=True)
+    _PINNED.append(t)
+    v = t.numpy()[: a.nbytes].view(a.dtype)
     v[:] = a
-    v._pin_owner = t  # noqa: keep the pinned storage alive
     return v
 
 

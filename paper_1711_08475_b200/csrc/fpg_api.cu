@@ -680,7 +680,8 @@ int fpg_dict_create(const uint8_t* bytes, const uint64_t* offsets, uint64_t n, c
     return guarded([&] {
         validate(scheme);
         if (!out) throw Error(FPG_EINVAL, "null output handle");
-        if (n && (!offsets || !bytes)) throw Error(FPG_EINVAL, "null dictionary buffers");
+        if (n && !offsets) throw Error(FPG_EINVAL, "null dictionary offsets");
+        if (n && offsets[n] > offsets[0] && !bytes) throw Error(FPG_EINVAL, "null dictionary bytes");
         if (n >= (1ull << 32) - 1) throw Error(FPG_EINVAL, "dictionary too large for 32-bit ids");
         if (id_base + n > (1ull << 32)) throw Error(FPG_EINVAL, "id_base + n exceeds 32-bit ids");
         std::vector<int32_t> devs;
@@ -769,7 +770,8 @@ int fpg_build_fingerprints(const uint8_t* bytes, const uint64_t* offsets, uint64
                            int32_t device, uint64_t* out) {
     return guarded([&] {
         validate(scheme);
-        if (n && (!bytes || !offsets || !out)) throw Error(FPG_EINVAL, "null argument");
+        if (n && (!offsets || !out)) throw Error(FPG_EINVAL, "null argument");
+        if (n && offsets[n] > offsets[0] && !bytes) throw Error(FPG_EINVAL, "null bytes");
         CK(cudaSetDevice(device));
         if (!n) return;
         const fpg::SchemeParams P = make_params(*scheme);
