@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -131,6 +132,7 @@ fpg::SchemeParams make_params(const fpg_scheme& s) {
     P.full = W == 64 ? ~0ull : ((1ull << W) - 1);
     if (s.variant == FPG_COUNT) {
         for (int q = 0; q < W / P.b; ++q) P.mask_fold |= 1ull << (W - P.b * (q + 1));
+        P.onehot = (W == 16 && P.b == 2) ? 1 : 0;
     } else if (s.variant == FPG_POSITION) {
         P.slots = W / P.p;
         P.extra = W - P.slots * P.p;
@@ -175,6 +177,13 @@ bool supports(int variant, int metric) {
 
 uint64_t g_launches = 0;  // approximate, per process; per-run counts are exact below
 
+// The verifier's occurrence-signature pre-check (exact; see occurrence_sig)
+// can be switched off with FPG_SIG_PRECHECK=0 to compare both paths.
+const bool g_sig_precheck = [] {
+    const char* e = std::getenv("FPG_SIG_PRECHECK");
+    return !(e && e[0] == '0');
+}();
+
 // Strings of one collection, length-bucketed on one device.
 struct Collection {
     uint64_t n = 0;
@@ -182,7 +191,9 @@ struct Collection {
     std::vector<uint64_t> byte_base;
     uint64_t total_bytes = 0;
     int max_len = 0;
-    DBuf<uint64_t> fp;
+    DBuf<uint64_t> fp;   // reference-layout fingerprints (prints())
+    DBuf<uint64_t> cmp;  // comparison words K2 reads (== fp, or the one-hot count-16 form)
+    DBuf<uint32_t> sig;  // occurrence signatures (verifier pre-check)
     DBuf<uint32_t> ids;
     DBuf<uint8_t> bytes;
     DBuf<uint32_t> d_start;
@@ -208,6 +219,8 @@ struct Collection {
         h_hist.reserve(L1 + 1);
         CK(cudaMemsetAsync(hist.p, 0, sizeof(uint32_t) * (L1 + 1), st));
         fp.reserve(n);
+        cmp.reserve(n);
+        sig.reserve(n);
         ids.reserve(n);
         if (n) {
             len_a.reserve(n); len_b.reserve(n); idx_a.reserve(n); idx_b.reserve(n);
@@ -246,10 +259,10 @@ struct Collection {
                                            end_bit, st));
         const unsigned grid = (unsigned)cdiv(n, 256);
         switch (P.variant) {
-            case 0: fpg::k_build<0><<<grid, 256, 0, st>>>(d_blob, d_offs, idx_b.p, n, d_start.p, d_byte_base.p, P, fp.p, ids.p, bytes.p); break;
-            case 1: fpg::k_build<1><<<grid, 256, 0, st>>>(d_blob, d_offs, idx_b.p, n, d_start.p, d_byte_base.p, P, fp.p, ids.p, bytes.p); break;
-            case 2: fpg::k_build<2><<<grid, 256, 0, st>>>(d_blob, d_offs, idx_b.p, n, d_start.p, d_byte_base.p, P, fp.p, ids.p, bytes.p); break;
-            default: fpg::k_build<3><<<grid, 256, 0, st>>>(d_blob, d_offs, idx_b.p, n, d_start.p, d_byte_base.p, P, fp.p, ids.p, bytes.p); break;
+            case 0: fpg::k_build<0><<<grid, 256, 0, st>>>(d_blob, d_offs, idx_b.p, n, d_start.p, d_byte_base.p, P, fp.p, cmp.p, sig.p, ids.p, bytes.p); break;
+            case 1: fpg::k_build<1><<<grid, 256, 0, st>>>(d_blob, d_offs, idx_b.p, n, d_start.p, d_byte_base.p, P, fp.p, cmp.p, sig.p, ids.p, bytes.p); break;
+            case 2: fpg::k_build<2><<<grid, 256, 0, st>>>(d_blob, d_offs, idx_b.p, n, d_start.p, d_byte_base.p, P, fp.p, cmp.p, sig.p, ids.p, bytes.p); break;
+            default: fpg::k_build<3><<<grid, 256, 0, st>>>(d_blob, d_offs, idx_b.p, n, d_start.p, d_byte_base.p, P, fp.p, cmp.p, sig.p, ids.p, bytes.p); break;
         }
         CK(cudaGetLastError());
         return launches + 1;
@@ -358,31 +371,47 @@ void for_each_shard(size_t n, F&& f) {
         if (codes[i]) throw Error(codes[i], "shard " + std::to_string(i) + ": " + errs[i]);
 }
 
-template <int VARIANT, int W>
-void launch_scan(const fpg::Tile* tiles, uint32_t ntiles, const fpg::ScanParams& P, int fold,
-                 cudaStream_t st, int device) {
+template <int KIND, int W, bool STATS>
+void launch_scan(const fpg::Tile* tiles, uint32_t ntiles, const fpg::ScanParams& P, cudaStream_t st,
+                 int device) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fpg::k_scan<VARIANT, W>, fpg::kScanThreads, 0));
-    const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)sms * std::max(per_sm, 1) * 4);
-    fpg::k_scan<VARIANT, W><<<(unsigned)std::max<uint64_t>(grid, 1), fpg::kScanThreads, 0, st>>>(tiles, ntiles, P, fold);
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fpg::k_scan<KIND, W, STATS>, fpg::kScanThreads, 0));
+    const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)sms * std::max(per_sm, 1) * 8);
+    fpg::k_scan<KIND, W, STATS><<<(unsigned)std::max<uint64_t>(grid, 1), fpg::kScanThreads, 0, st>>>(tiles, ntiles, P);
     CK(cudaGetLastError());
 }
 
-void dispatch_scan(int variant, int width, const fpg::Tile* tiles, uint32_t ntiles, const fpg::ScanParams& P,
-                   int fold, cudaStream_t st, int device) {
-#define FPG_W(V)                                                                           \
-    if (width == 16) launch_scan<V, 16>(tiles, ntiles, P, fold, st, device);               \
-    else if (width == 32) launch_scan<V, 32>(tiles, ntiles, P, fold, st, device);          \
-    else launch_scan<V, 64>(tiles, ntiles, P, fold, st, device);
-    switch (variant) {
-        case 0: FPG_W(0) break;
-        case 1: FPG_W(1) break;
-        case 2: FPG_W(2) break;
-        default: FPG_W(3) break;
+template <int KIND>
+void launch_w(int width, bool stats, const fpg::Tile* tiles, uint32_t ntiles, const fpg::ScanParams& P,
+              cudaStream_t st, int device) {
+    if (width == 16) stats ? launch_scan<KIND, 16, true>(tiles, ntiles, P, st, device)
+                           : launch_scan<KIND, 16, false>(tiles, ntiles, P, st, device);
+    else if (width == 32) stats ? launch_scan<KIND, 32, true>(tiles, ntiles, P, st, device)
+                                : launch_scan<KIND, 32, false>(tiles, ntiles, P, st, device);
+    else stats ? launch_scan<KIND, 64, true>(tiles, ntiles, P, st, device)
+               : launch_scan<KIND, 64, false>(tiles, ntiles, P, st, device);
+}
+
+// Distance form per scheme: plain popcount (occurrence, halved, one-hot
+// count-16), compile-time folds for count b=2/4 and position p=3, else the
+// generic runtime fold.
+int dist_kind(const fpg::SchemeParams& S) {
+    if (S.variant == FPG_OCCURRENCE || S.variant == FPG_OCCURRENCE_HALVED || S.onehot) return fpg::kPopc;
+    if (S.variant == FPG_COUNT) return S.b == 2 ? fpg::kFold2 : S.b == 4 ? fpg::kFold4 : fpg::kGeneric;
+    return S.p == 3 ? fpg::kPos3 : fpg::kGeneric;
+}
+
+void dispatch_scan(const fpg::SchemeParams& S, bool stats, const fpg::Tile* tiles, uint32_t ntiles,
+                   const fpg::ScanParams& P, cudaStream_t st, int device) {
+    switch (dist_kind(S)) {
+        case fpg::kPopc: launch_w<fpg::kPopc>(S.width, stats, tiles, ntiles, P, st, device); break;
+        case fpg::kFold2: launch_w<fpg::kFold2>(S.width, stats, tiles, ntiles, P, st, device); break;
+        case fpg::kFold4: launch_w<fpg::kFold4>(S.width, stats, tiles, ntiles, P, st, device); break;
+        case fpg::kPos3: launch_w<fpg::kPos3>(S.width, stats, tiles, ntiles, P, st, device); break;
+        default: launch_w<fpg::kGeneric>(S.width, stats, tiles, ntiles, P, st, device); break;
     }
-#undef FPG_W
 }
 
 bool compatible(int metric, int k, int lq, int lw) {
@@ -444,10 +473,13 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
     S.counters.reserve(2);
     S.h_counters.reserve(2);
     fpg::ScanParams P{};
-    P.q_fp = Q.fp.p;
+    P.q_fp = Q.cmp.p;
     P.q_bytes = Q.bytes.p;
     P.q_ids = Q.ids.p;
-    P.w_fp = W.fp.p;
+    P.w_fp = W.cmp.p;
+    P.q_sig = Q.sig.p;
+    P.w_sig = W.sig.p;
+    P.sig_thr = g_sig_precheck ? 2 * o.k : 64;
     P.w_bytes = W.bytes.p;
     P.w_ids = W.ids.p;
     P.id_base = D->id_base + sh.base;
@@ -456,10 +488,12 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
     P.survivors_total = S.counters.p + 1;
     P.mask_fold = D->params.mask_fold;
     P.mask_single = D->params.mask_single;
-    P.thr = o.use_filter ? 2 * o.k : 1 << 20;
+    // reject iff F_D > 2k (ceil_half(F_D) > k, dictionary.hpp:102-106); the
+    // one-hot count form counts every differing field twice
+    P.thr = o.use_filter ? (D->params.onehot ? 4 * o.k : 2 * o.k) : 1 << 20;
     P.k = o.k;
-    const int fold = D->params.variant == FPG_COUNT ? D->params.b
-                   : D->params.variant == FPG_POSITION ? D->params.p : 1;
+    P.fold = D->params.variant == FPG_COUNT ? D->params.b
+           : D->params.variant == FPG_POSITION ? D->params.p : 1;
     for (;;) {
         S.out.reserve(S.out_cap);
         P.out = S.out.p;
@@ -468,7 +502,7 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         if (nq) CK(cudaMemsetAsync(S.qsurv.p, 0, nq * sizeof(uint32_t), st));
         CK(cudaEventRecord(S.ev[1], st));
         if (!plan.empty()) {
-            dispatch_scan(D->params.variant, D->params.width, S.tiles.p, (uint32_t)plan.size(), P, fold, st, sh.device);
+            dispatch_scan(D->params, o.want_stats != 0, S.tiles.p, (uint32_t)plan.size(), P, st, sh.device);
             ++S.launches;
         }
         CK(cudaEventRecord(S.ev[2], st));
@@ -794,10 +828,10 @@ int fpg_build_fingerprints(const uint8_t* bytes, const uint64_t* offsets, uint64
         CK(cudaMemcpyAsync(offs.p, local.data(), (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
         const unsigned grid = (unsigned)cdiv(n, 256);
         switch (P.variant) {
-            case 0: fpg::k_build<0><<<grid, 256, 0, st>>>(blob.p, offs.p, nullptr, n, nullptr, nullptr, P, fp.p, nullptr, nullptr); break;
-            case 1: fpg::k_build<1><<<grid, 256, 0, st>>>(blob.p, offs.p, nullptr, n, nullptr, nullptr, P, fp.p, nullptr, nullptr); break;
-            case 2: fpg::k_build<2><<<grid, 256, 0, st>>>(blob.p, offs.p, nullptr, n, nullptr, nullptr, P, fp.p, nullptr, nullptr); break;
-            default: fpg::k_build<3><<<grid, 256, 0, st>>>(blob.p, offs.p, nullptr, n, nullptr, nullptr, P, fp.p, nullptr, nullptr); break;
+            case 0: fpg::k_build<0><<<grid, 256, 0, st>>>(blob.p, offs.p, nullptr, n, nullptr, nullptr, P, fp.p, nullptr, nullptr, nullptr, nullptr); break;
+            case 1: fpg::k_build<1><<<grid, 256, 0, st>>>(blob.p, offs.p, nullptr, n, nullptr, nullptr, P, fp.p, nullptr, nullptr, nullptr, nullptr); break;
+            case 2: fpg::k_build<2><<<grid, 256, 0, st>>>(blob.p, offs.p, nullptr, n, nullptr, nullptr, P, fp.p, nullptr, nullptr, nullptr, nullptr); break;
+            default: fpg::k_build<3><<<grid, 256, 0, st>>>(blob.p, offs.p, nullptr, n, nullptr, nullptr, P, fp.p, nullptr, nullptr, nullptr, nullptr); break;
         }
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(out, fp.p, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));

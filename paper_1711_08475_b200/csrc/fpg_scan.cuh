@@ -1,0 +1,343 @@
+// fpg_scan.cuh -- K2: the fused filter + k<=1 verify scan (sm_100a).
+//
+// One CTA = 8 warps = one tile: up to 2048 words of one dictionary length
+// bucket (8 per lane, comparison words in registers) x up to 256 queries of
+// one query length bucket (comparison words in shared memory, read as warp
+// broadcasts).  For every (query, word) pair the reference's fingerprint test
+// (dictionary.hpp:102-106: ceil_half(F_D) > k, i.e. F_D > 2k) runs as one
+// XOR + POPC (+ a compile-time field fold for count / position layouts,
+// ComparisonTables fingerprint.hpp:180-194).  Survivors are appended without
+// any warp vote to a lane-private queue in shared memory (slot-major
+// [slot][lane] layout: conflict-free), and when any lane's queue is nearly
+// full the warp verifies all queued candidates slot by slot with register-
+// resident byte compares (hamming_bounded / levenshtein_bounded at k<=1,
+// edit_distance.hpp:18-64).  Matches (rare) leave through a warp-aggregated
+// atomic append; per-query survivor counts (QueryStats::verified) come from
+// one REDUX per warp and query.
+#pragma once
+
+#include <cstdint>
+#include <type_traits>
+
+namespace fpg {
+
+enum DistKind : int { kPopc = 0, kFold2 = 1, kFold4 = 2, kPos3 = 3, kGeneric = 4 };
+
+template <typename T>
+__device__ __forceinline__ int popcnt(T x) {
+    if constexpr (sizeof(T) == 8) return __popcll(x);
+    else return __popc(x);
+}
+
+// F_D on the comparison words' xor.  kPopc covers occurrence, halved and the
+// one-hot count-16 form (whose popcount is twice F_D; the threshold is doubled
+// on the host instead).
+template <int KIND, typename T>
+__device__ __forceinline__ int distance_of(T x, T mf, T ms, int fold) {
+    if constexpr (KIND == kPopc) {
+        return popcnt(x);
+    } else if constexpr (KIND == kFold2) {
+        return popcnt((x | (x >> 1)) & mf);
+    } else if constexpr (KIND == kFold4) {
+        return popcnt((x | (x >> 1) | (x >> 2) | (x >> 3)) & mf);
+    } else if constexpr (KIND == kPos3) {
+        return popcnt(((x | (x >> 1) | (x >> 2)) & mf) | (x & ms));
+    } else {
+        T f = x;
+        for (int j = 1; j < fold; ++j) f |= x >> j;
+        return popcnt((f & mf) | (x & ms));
+    }
+}
+
+__device__ __forceinline__ uint32_t ld32(const uint8_t* base, int chunk, int stride) {
+    return (4 * chunk < stride) ? __ldg(reinterpret_cast<const uint32_t*>(base) + chunk) : 0u;
+}
+
+// k<=1 verification of zero-padded byte strings, any length (global loads).
+// Semantics of hamming_bounded / levenshtein_bounded (edit_distance.hpp:18-64):
+//   equal lengths: distance <= 1  <=>  first mismatching byte == last one;
+//   lengths differ by one (long s, short t): t is s with one byte deleted  <=>
+//   (last mismatch of t vs s shifted left by one byte) < (first mismatch of t vs s).
+__device__ __forceinline__ bool verify_pair(const uint8_t* q, int m, int qs, const uint8_t* w,
+                                            int n, int ws, int k) {
+    const int d = n - m;
+    if (d == 0) {
+        const int nc = (m + 3) >> 2;
+        int first = 1 << 30, last = -1;
+        for (int c = 0; c < nc; ++c) {
+            const uint32_t x = ld32(q, c, qs) ^ ld32(w, c, ws);
+            if (x) {
+                if (first == (1 << 30)) first = 4 * c + ((__ffs(x) - 1) >> 3);
+                last = 4 * c + ((31 - __clz(x)) >> 3);
+                if (k == 0 || last != first) return false;
+            }
+        }
+        return true;
+    }
+    if (k == 0) return false;
+    const uint8_t* s = d > 0 ? w : q;
+    const uint8_t* t = d > 0 ? q : w;
+    const int ss = d > 0 ? ws : qs, ts = d > 0 ? qs : ws;
+    const int nc = ((d > 0 ? n : m) + 3) >> 2;
+    int firstA = 1 << 30, lastB = -1;
+    uint32_t s0 = ld32(s, 0, ss);
+    for (int c = 0; c < nc; ++c) {
+        const uint32_t s1 = ld32(s, c + 1, ss);
+        const uint32_t tc = ld32(t, c, ts);
+        const uint32_t xa = tc ^ s0;
+        const uint32_t xb = tc ^ __funnelshift_r(s0, s1, 8);
+        if (xa && firstA == (1 << 30)) firstA = 4 * c + ((__ffs(xa) - 1) >> 3);
+        if (xb) lastB = 4 * c + ((31 - __clz(xb)) >> 3);
+        s0 = s1;
+    }
+    return lastB < firstA;
+}
+
+// Same test with both strings already in registers (NW 32-bit words, zero
+// padded, NW*4 >= max(m, n)).
+template <int NW>
+__device__ __forceinline__ bool verify_regs(const uint32_t (&q)[NW], const uint32_t (&w)[NW], int m,
+                                            int n, int k) {
+    if (m == n) {
+        int fi = NW, li = -1;
+        uint32_t fx = 0, lx = 0;
+#pragma unroll
+        for (int i = NW - 1; i >= 0; --i) {
+            const uint32_t x = q[i] ^ w[i];
+            if (x) { fi = i; fx = x; }
+        }
+        if (fi == NW) return true;
+        if (k == 0) return false;
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+            const uint32_t x = q[i] ^ w[i];
+            if (x) { li = i; lx = x; }
+        }
+        return fi == li && ((__ffs(fx) - 1) >> 3) == ((31 - __clz(lx)) >> 3);
+    }
+    if (k == 0) return false;
+    const bool wl = n > m;  // tile-uniform
+    int fi = NW, li = -1;
+    uint32_t fx = 0, lx = 0;
+#pragma unroll
+    for (int i = NW - 1; i >= 0; --i) {
+        const uint32_t a = q[i] ^ w[i];
+        if (a) { fi = i; fx = a; }
+    }
+    if (fi == NW) return true;  // shorter is a prefix of longer (and the extra byte is 0)
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+        const uint32_t s0 = wl ? w[i] : q[i];
+        const uint32_t s1 = (i + 1 < NW) ? (wl ? w[i + 1] : q[i + 1]) : 0u;
+        const uint32_t t0 = wl ? q[i] : w[i];
+        const uint32_t b = t0 ^ __funnelshift_r(s0, s1, 8);
+        if (b) { li = i; lx = b; }
+    }
+    if (li < 0) return true;
+    const int fa = 4 * fi + ((__ffs(fx) - 1) >> 3);
+    const int lb = 4 * li + ((31 - __clz(lx)) >> 3);
+    return lb < fa;
+}
+
+template <int NW>
+__device__ __forceinline__ void load_padded(const uint8_t* p, int stride, uint32_t (&r)[NW]) {
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(p));
+    r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w;
+    if constexpr (NW == 8) {
+        uint4 b = make_uint4(0, 0, 0, 0);
+        if (stride > 16) b = __ldg(reinterpret_cast<const uint4*>(p) + 1);
+        r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
+    }
+}
+
+constexpr int kScanThreads = 256;
+constexpr int kScanWarps = kScanThreads / 32;
+constexpr int kWordsPerLane = 8;                                   // R
+constexpr int kTileWords = kScanThreads * kWordsPerLane;           // 2048
+constexpr int kTileQueries = 256;
+constexpr int kLaneCap = 24;                                       // queue slots per lane
+
+// Per-tile state of one warp (all members live in registers once inlined).
+template <int KIND, typename T, bool STATS>
+struct TileScan {
+    const ScanParams& P;
+    const Tile& tl;
+    uint32_t* s_queue;
+    const uint32_t* s_qsig;
+    const uint32_t* s_wsig;
+    const uint8_t* qbytes;
+    const uint8_t* wbytes;
+    int m, n, qs, ws, vclass, tid, lane;
+    uint32_t qhead, qlimit, qp;
+    unsigned long long* surv_lane;
+
+    __device__ __forceinline__ bool verify_bytes(uint32_t j, uint32_t widx) const {
+        const uint8_t* qb = qbytes + (uint64_t)j * qs;
+        const uint8_t* wb = wbytes + (uint64_t)widx * ws;
+        if (vclass == 1) {
+            uint32_t a[4], b[4];
+            load_padded<4>(qb, qs, a);
+            load_padded<4>(wb, ws, b);
+            return verify_regs<4>(a, b, m, n, P.k);
+        }
+        if (vclass == 2) {
+            uint32_t a[8], b[8];
+            load_padded<8>(qb, qs, a);
+            load_padded<8>(wb, ws, b);
+            return verify_regs<8>(a, b, m, n, P.k);
+        }
+        return verify_pair(qb, m, qs, wb, n, ws, P.k);
+    }
+
+    // Verifies every queued (query, survivor mask) entry of the warp: the
+    // signature pre-check per survivor, then byte compares for the rest.
+    __device__ __forceinline__ void flush() {
+        __syncwarp();
+        const uint32_t lt_mask = (1u << lane) - 1u;
+        const int cnt = (int)((qp - qhead) >> 5);
+        const int maxc = (int)__reduce_max_sync(0xffffffffu, (unsigned)cnt);
+        for (int s = 0; s < maxc; ++s) {
+            uint32_t e = 0;
+            if (s < cnt) e = s_queue[qhead + 32 * s];
+            const uint32_t j = e >> 8;
+            uint32_t msk = e & 0xffu;
+            if (msk) {
+                *surv_lane += (unsigned)__popc(msk);
+                const uint32_t qg = s_qsig[j];
+                uint32_t keep = 0;
+                do {
+                    const int r = __ffs(msk) - 1;
+                    msk &= msk - 1;
+                    if (__popc(qg ^ s_wsig[r * kScanThreads + tid]) <= P.sig_thr) keep |= 1u << r;
+                } while (msk);
+                msk = keep;
+            }
+            while (__any_sync(0xffffffffu, msk != 0)) {
+                bool hit = false;
+                uint32_t widx = 0;
+                if (msk) {
+                    const int r = __ffs(msk) - 1;
+                    msk &= msk - 1;
+                    widx = (uint32_t)(r * kScanThreads + tid);
+                    hit = verify_bytes(j, widx);
+                }
+                const uint32_t hb = __ballot_sync(0xffffffffu, hit);
+                if (hb) {
+                    unsigned long long slot = 0;
+                    if (lane == 0) slot = atomicAdd(P.out_count, (unsigned long long)__popc(hb));
+                    slot = __shfl_sync(0xffffffffu, slot, 0);
+                    if (hit) {
+                        const uint64_t o = slot + __popc(hb & lt_mask);
+                        if (o < P.out_cap) {
+                            const uint64_t qid = P.q_ids[tl.q_begin + j];
+                            const uint64_t wid = P.id_base + P.w_ids[tl.w_begin + widx];
+                            P.out[o] = (qid << 32) | wid;
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        qp = qhead;
+    }
+
+    // Filter loop over the tile's queries.  FULL: all 8 words of every lane
+    // are valid (all but each bucket's last tile), so no validity predicates.
+    template <bool FULL>
+    __device__ __forceinline__ void scan(const T* s_q, const T (&wc)[kWordsPerLane], const bool (&wv)[kWordsPerLane],
+                                         uint32_t* s_wsurv_warp) {
+        const T mf = (T)P.mask_fold, ms = (T)P.mask_single;
+        const int thr = P.thr;
+        for (uint32_t j = 0; j < tl.q_count; ++j) {
+            const T qc = s_q[j];
+            uint32_t msk = 0;
+#pragma unroll
+            for (int r = 0; r < kWordsPerLane; ++r) {
+                bool pass = distance_of<KIND, T>(qc ^ wc[r], mf, ms, P.fold) <= thr;
+                if constexpr (!FULL) pass &= wv[r];
+                msk |= pass ? (1u << r) : 0u;
+            }
+            s_queue[qp] = (j << 8) | msk;  // unconditional: the slot is free until qp moves
+            qp += msk ? 32u : 0u;
+            if constexpr (STATS) {
+                const unsigned c = __reduce_add_sync(0xffffffffu, (unsigned)__popc(msk));
+                if (lane == 0) s_wsurv_warp[j] = c;
+            }
+            if (__any_sync(0xffffffffu, qp > qlimit)) flush();
+        }
+        flush();
+    }
+};
+
+template <int KIND, int W, bool STATS>
+__global__ void __launch_bounds__(kScanThreads, 4) k_scan(const Tile* __restrict__ tiles, uint32_t ntiles,
+                                                       const __grid_constant__ ScanParams P) {
+    using T = typename std::conditional<(W <= 32), uint32_t, uint64_t>::type;
+    __shared__ T s_q[kTileQueries];
+    __shared__ uint32_t s_qsig[kTileQueries];
+    __shared__ uint32_t s_wsig[kWordsPerLane * kScanThreads];
+    __shared__ uint32_t s_wsurv[STATS ? kScanWarps : 1][STATS ? kTileQueries : 1];
+    __shared__ uint32_t s_queue[kScanWarps * kLaneCap * 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // lane-private queue, slot-major: slot s of this lane at qhead + 32 s
+    const uint32_t qhead = (uint32_t)(warp * kLaneCap * 32 + lane);
+    unsigned long long surv_lane = 0;
+
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const Tile tl = tiles[t];
+        __syncthreads();  // previous tile's shared state fully consumed
+        for (uint32_t i = tid; i < tl.q_count; i += kScanThreads) {
+            s_q[i] = (T)P.q_fp[tl.q_begin + i];
+            s_qsig[i] = P.q_sig[tl.q_begin + i];
+        }
+        T wc[kWordsPerLane];
+        bool wv[kWordsPerLane];
+#pragma unroll
+        for (int r = 0; r < kWordsPerLane; ++r) {
+            const uint32_t widx = r * kScanThreads + tid;
+            wv[r] = widx < tl.w_count;
+            wc[r] = wv[r] ? (T)P.w_fp[tl.w_begin + widx] : (T)0;
+            s_wsig[widx] = wv[r] ? P.w_sig[tl.w_begin + widx] : 0u;
+        }
+        __syncthreads();
+
+        if (!tl.count_only) {
+            TileScan<KIND, T, STATS> ts{P, tl, s_queue, s_qsig, s_wsig,
+                                        P.q_bytes + tl.q_bytes, P.w_bytes + tl.w_bytes,
+                                        tl.q_len, tl.w_len, tl.q_stride, tl.w_stride,
+                                        (tl.q_len <= 16 && tl.w_len <= 16) ? 1 : (tl.q_len <= 32 && tl.w_len <= 32) ? 2 : 0,
+                                        tid, lane, qhead, qhead + (uint32_t)(kLaneCap - 1) * 32, qhead, &surv_lane};
+            if (tl.w_count == kTileWords) ts.template scan<true>(s_q, wc, wv, s_wsurv[STATS ? warp : 0]);
+            else ts.template scan<false>(s_q, wc, wv, s_wsurv[STATS ? warp : 0]);
+        } else if constexpr (STATS) {
+            // incompatible lengths with the length prefilter off: the reference
+            // still runs the fingerprint test (dictionary.hpp:102-106) and
+            // counts survivors as verified; the verifier rejects them by length.
+            const T mf = (T)P.mask_fold, ms = (T)P.mask_single;
+            for (uint32_t j = 0; j < tl.q_count; ++j) {
+                const T qc = s_q[j];
+                unsigned c = 0;
+#pragma unroll
+                for (int r = 0; r < kWordsPerLane; ++r)
+                    c += ((distance_of<KIND, T>(qc ^ wc[r], mf, ms, P.fold) <= P.thr) & wv[r]) ? 1u : 0u;
+                c = __reduce_add_sync(0xffffffffu, c);
+                if (lane == 0) s_wsurv[warp][j] = c;
+                surv_lane += lane == 0 ? c : 0;
+            }
+        }
+        if constexpr (STATS) {
+            __syncthreads();
+            for (uint32_t i = tid; i < tl.q_count; i += kScanThreads) {
+                uint32_t v = 0;
+#pragma unroll
+                for (int w = 0; w < kScanWarps; ++w) v += s_wsurv[w][i];
+                if (v) atomicAdd(&P.q_survivors[P.q_ids[tl.q_begin + i]], v);
+            }
+        }
+    }
+    // run total of fingerprint survivors (for reporting), one atomic per warp
+    for (int o = 16; o; o >>= 1) surv_lane += __shfl_xor_sync(0xffffffffu, surv_lane, o);
+    if (lane == 0 && surv_lane) atomicAdd(P.survivors_total, surv_lane);
+}
+
+}  // namespace fpg
