@@ -157,19 +157,50 @@ constexpr int kTileWords = kScanThreads * kWordsPerLane;           // 2048
 constexpr int kTileQueries = 256;
 constexpr int kLaneCap = 24;                                       // queue slots per lane
 
+// 32-bit shared-window addressing (keeps generic->shared conversions out of loops).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ T lds_t(uint32_t a) {
+    if constexpr (sizeof(T) == 8) {
+        uint64_t v;
+        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+        return v;
+    } else {
+        return lds32(a);
+    }
+}
+
+// popc(x) <= t for t in {0, 2} without the XU pipe (clear the lowest set bit twice).
+__device__ __forceinline__ bool popc_le(uint32_t x, int t) {
+    if (t >= 32) return true;
+    if (t == 0) return x == 0;
+    const uint32_t y = x & (x - 1);
+    if (t == 1) return y == 0;
+    return (y & (y - 1)) == 0 || t > 2;
+}
+
 // Per-tile state of one warp (all members live in registers once inlined).
 template <int KIND, typename T, bool STATS>
 struct TileScan {
     const ScanParams& P;
     const Tile& tl;
-    uint32_t* s_queue;
-    const uint32_t* s_qsig;
-    const uint32_t* s_wsig;
     const uint8_t* qbytes;
     const uint8_t* wbytes;
     int m, n, qs, ws, vclass, tid, lane;
-    uint32_t qhead, qlimit, qp;
-    unsigned long long* surv_lane;
+    uint32_t a_queue;    // shared address of this lane's queue slot 0 (slot s at + 128 s)
+    uint32_t a_qlimit;   // flush once the next push could pass the last slot
+    uint32_t a_qsig;
+    uint32_t qp;
 
     __device__ __forceinline__ bool verify_bytes(uint32_t j, uint32_t widx) const {
         const uint8_t* qb = qbytes + (uint64_t)j * qs;
@@ -189,36 +220,27 @@ struct TileScan {
         return verify_pair(qb, m, qs, wb, n, ws, P.k);
     }
 
-    // Verifies every queued (query, survivor mask) entry of the warp: the
-    // signature pre-check per survivor, then byte compares for the rest.
+    // Verifies every queued entry of the warp by byte compares.  Entry =
+    // (j << 16) | mask(j+1) << 8 | mask(j): pairs of queries j, j+1 with this
+    // lane's 8 words that passed both the fingerprint and the signature test.
     __device__ __forceinline__ void flush() {
         __syncwarp();
         const uint32_t lt_mask = (1u << lane) - 1u;
-        const int cnt = (int)((qp - qhead) >> 5);
+        const int cnt = (int)((qp - a_queue) >> 7);
         const int maxc = (int)__reduce_max_sync(0xffffffffu, (unsigned)cnt);
         for (int s = 0; s < maxc; ++s) {
             uint32_t e = 0;
-            if (s < cnt) e = s_queue[qhead + 32 * s];
-            const uint32_t j = e >> 8;
-            uint32_t msk = e & 0xffu;
-            if (msk) {
-                *surv_lane += (unsigned)__popc(msk);
-                const uint32_t qg = s_qsig[j];
-                uint32_t keep = 0;
-                do {
-                    const int r = __ffs(msk) - 1;
-                    msk &= msk - 1;
-                    if (__popc(qg ^ s_wsig[r * kScanThreads + tid]) <= P.sig_thr) keep |= 1u << r;
-                } while (msk);
-                msk = keep;
-            }
-            while (__any_sync(0xffffffffu, msk != 0)) {
+            if (s < cnt) e = lds32(a_queue + 128u * s);
+            const uint32_t j0 = e >> 16;
+            uint32_t keep = e & 0xffffu;
+            while (__any_sync(0xffffffffu, keep != 0)) {
                 bool hit = false;
-                uint32_t widx = 0;
-                if (msk) {
-                    const int r = __ffs(msk) - 1;
-                    msk &= msk - 1;
-                    widx = (uint32_t)(r * kScanThreads + tid);
+                uint32_t j = 0, widx = 0;
+                if (keep) {
+                    const int b = 31 - __clz(keep);
+                    keep ^= 1u << b;
+                    j = j0 + (b >> 3);
+                    widx = (uint32_t)((b & 7) * kScanThreads + tid);
                     hit = verify_bytes(j, widx);
                 }
                 const uint32_t hb = __ballot_sync(0xffffffffu, hit);
@@ -238,50 +260,79 @@ struct TileScan {
             }
         }
         __syncwarp();
-        qp = qhead;
+        qp = a_queue;
     }
 
-    // Filter loop over the tile's queries.  FULL: all 8 words of every lane
-    // are valid (all but each bucket's last tile), so no validity predicates.
+    // Filter loop over the tile's queries, two per iteration.  Per pair: the
+    // reference fingerprint test (counted for QueryStats) and the exact
+    // occurrence-signature test; pairs passing both are queued.  The
+    // signature popcount runs on the XU pipe for words 0..4 and as ALU
+    // bit-clears for words 5..7, balancing the two pipes.  FULL: all 8 words
+    // of every lane are valid (all but each bucket's last tile).  Returns the
+    // warp's fingerprint-survivor count (STATS only).
     template <bool FULL>
-    __device__ __forceinline__ void scan(const T* s_q, const T (&wc)[kWordsPerLane], const bool (&wv)[kWordsPerLane],
-                                         uint32_t* s_wsurv_warp) {
+    __device__ __forceinline__ unsigned scan(uint32_t a_q, const T (&wc)[kWordsPerLane],
+                                             const uint32_t (&wg)[kWordsPerLane],
+                                             const bool (&wv)[kWordsPerLane], uint32_t a_wsurv) {
         const T mf = (T)P.mask_fold, ms = (T)P.mask_single;
-        const int thr = P.thr;
-        for (uint32_t j = 0; j < tl.q_count; ++j) {
-            const T qc = s_q[j];
-            uint32_t msk = 0;
+        const int thr = P.thr, sthr = P.sig_thr;
+        unsigned total = 0;
+        for (uint32_t j = 0; j < tl.q_count; j += 2) {
+            const bool two = j + 1 < tl.q_count;
+            const uint32_t j1 = two ? j + 1 : j;
+            const T q0 = lds_t<T>(a_q + (uint32_t)sizeof(T) * j);
+            const T q1 = lds_t<T>(a_q + (uint32_t)sizeof(T) * j1);
+            const uint32_t g0 = lds32(a_qsig + 4u * j);
+            const uint32_t g1 = lds32(a_qsig + 4u * j1);
+            uint32_t mfp = 0, mboth = 0;
 #pragma unroll
             for (int r = 0; r < kWordsPerLane; ++r) {
-                bool pass = distance_of<KIND, T>(qc ^ wc[r], mf, ms, P.fold) <= thr;
-                if constexpr (!FULL) pass &= wv[r];
-                msk |= pass ? (1u << r) : 0u;
+                bool f0 = distance_of<KIND, T>(q0 ^ wc[r], mf, ms, P.fold) <= thr;
+                bool f1 = distance_of<KIND, T>(q1 ^ wc[r], mf, ms, P.fold) <= thr;
+                if constexpr (!FULL) { f0 &= wv[r]; f1 &= wv[r]; }
+                bool s0, s1;
+                if (r < 5) {
+                    s0 = __popc(g0 ^ wg[r]) <= sthr;
+                    s1 = __popc(g1 ^ wg[r]) <= sthr;
+                } else {
+                    s0 = popc_le(g0 ^ wg[r], sthr);
+                    s1 = popc_le(g1 ^ wg[r], sthr);
+                }
+                mfp |= (f0 ? (1u << r) : 0u) | (f1 ? (0x100u << r) : 0u);
+                mboth |= ((f0 & s0) ? (1u << r) : 0u) | ((f1 & s1) ? (0x100u << r) : 0u);
             }
-            s_queue[qp] = (j << 8) | msk;  // unconditional: the slot is free until qp moves
-            qp += msk ? 32u : 0u;
+            if (!two) { mfp &= 0xffu; mboth &= 0xffu; }
+            sts32(qp, (j << 16) | mboth);  // unconditional: the slot is free until qp moves
+            qp += mboth ? 128u : 0u;
             if constexpr (STATS) {
-                const unsigned c = __reduce_add_sync(0xffffffffu, (unsigned)__popc(msk));
-                if (lane == 0) s_wsurv_warp[j] = c;
+                const unsigned c = __reduce_add_sync(0xffffffffu, (unsigned)(__popc(mfp & 0xffu) | (__popc(mfp >> 8) << 16)));
+                if (lane == 0) {
+                    sts32(a_wsurv + 4u * j, c & 0xffffu);
+                    if (two) sts32(a_wsurv + 4u * j1, c >> 16);
+                }
+                total += (c & 0xffffu) + (c >> 16);
             }
-            if (__any_sync(0xffffffffu, qp > qlimit)) flush();
+            if (__any_sync(0xffffffffu, qp > a_qlimit)) flush();
         }
         flush();
+        return total;
     }
 };
 
 template <int KIND, int W, bool STATS>
 __global__ void __launch_bounds__(kScanThreads, 4) k_scan(const Tile* __restrict__ tiles, uint32_t ntiles,
-                                                       const __grid_constant__ ScanParams P) {
+                                                          const __grid_constant__ ScanParams P) {
     using T = typename std::conditional<(W <= 32), uint32_t, uint64_t>::type;
     __shared__ T s_q[kTileQueries];
     __shared__ uint32_t s_qsig[kTileQueries];
-    __shared__ uint32_t s_wsig[kWordsPerLane * kScanThreads];
     __shared__ uint32_t s_wsurv[STATS ? kScanWarps : 1][STATS ? kTileQueries : 1];
     __shared__ uint32_t s_queue[kScanWarps * kLaneCap * 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // lane-private queue, slot-major: slot s of this lane at qhead + 32 s
-    const uint32_t qhead = (uint32_t)(warp * kLaneCap * 32 + lane);
-    unsigned long long surv_lane = 0;
+    // lane-private queue, slot-major: slot s of this lane at word (warp*cap + s)*32 + lane
+    const uint32_t a_queue = smem_u32(s_queue) + 4u * (uint32_t)(warp * kLaneCap * 32 + lane);
+    const uint32_t a_q = smem_u32(s_q), a_qsig = smem_u32(s_qsig);
+    const uint32_t a_wsurv = smem_u32(s_wsurv[STATS ? warp : 0]);
+    unsigned long long surv_warp = 0;  // lane 0's copy is the warp total (STATS)
 
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const Tile tl = tiles[t];
@@ -291,24 +342,24 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(const Tile* __restrict
             s_qsig[i] = P.q_sig[tl.q_begin + i];
         }
         T wc[kWordsPerLane];
+        uint32_t wg[kWordsPerLane];
         bool wv[kWordsPerLane];
 #pragma unroll
         for (int r = 0; r < kWordsPerLane; ++r) {
             const uint32_t widx = r * kScanThreads + tid;
             wv[r] = widx < tl.w_count;
             wc[r] = wv[r] ? (T)P.w_fp[tl.w_begin + widx] : (T)0;
-            s_wsig[widx] = wv[r] ? P.w_sig[tl.w_begin + widx] : 0u;
+            wg[r] = wv[r] ? P.w_sig[tl.w_begin + widx] : 0u;
         }
         __syncthreads();
 
         if (!tl.count_only) {
-            TileScan<KIND, T, STATS> ts{P, tl, s_queue, s_qsig, s_wsig,
-                                        P.q_bytes + tl.q_bytes, P.w_bytes + tl.w_bytes,
+            TileScan<KIND, T, STATS> ts{P, tl, P.q_bytes + tl.q_bytes, P.w_bytes + tl.w_bytes,
                                         tl.q_len, tl.w_len, tl.q_stride, tl.w_stride,
                                         (tl.q_len <= 16 && tl.w_len <= 16) ? 1 : (tl.q_len <= 32 && tl.w_len <= 32) ? 2 : 0,
-                                        tid, lane, qhead, qhead + (uint32_t)(kLaneCap - 1) * 32, qhead, &surv_lane};
-            if (tl.w_count == kTileWords) ts.template scan<true>(s_q, wc, wv, s_wsurv[STATS ? warp : 0]);
-            else ts.template scan<false>(s_q, wc, wv, s_wsurv[STATS ? warp : 0]);
+                                        tid, lane, a_queue, a_queue + 128u * (kLaneCap - 1), a_qsig, a_queue};
+            surv_warp += (tl.w_count == kTileWords) ? ts.template scan<true>(a_q, wc, wg, wv, a_wsurv)
+                                                    : ts.template scan<false>(a_q, wc, wg, wv, a_wsurv);
         } else if constexpr (STATS) {
             // incompatible lengths with the length prefilter off: the reference
             // still runs the fingerprint test (dictionary.hpp:102-106) and
@@ -322,7 +373,7 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(const Tile* __restrict
                     c += ((distance_of<KIND, T>(qc ^ wc[r], mf, ms, P.fold) <= P.thr) & wv[r]) ? 1u : 0u;
                 c = __reduce_add_sync(0xffffffffu, c);
                 if (lane == 0) s_wsurv[warp][j] = c;
-                surv_lane += lane == 0 ? c : 0;
+                surv_warp += c;
             }
         }
         if constexpr (STATS) {
@@ -335,9 +386,8 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(const Tile* __restrict
             }
         }
     }
-    // run total of fingerprint survivors (for reporting), one atomic per warp
-    for (int o = 16; o; o >>= 1) surv_lane += __shfl_xor_sync(0xffffffffu, surv_lane, o);
-    if (lane == 0 && surv_lane) atomicAdd(P.survivors_total, surv_lane);
+    // run total of fingerprint survivors (reported), one atomic per warp
+    if (STATS && lane == 0 && surv_warp) atomicAdd(P.survivors_total, surv_warp);
 }
 
 }  // namespace fpg
