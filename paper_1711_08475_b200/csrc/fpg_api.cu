@@ -265,6 +265,8 @@ struct Collection {
             default: fpg::k_build<3><<<grid, 256, 0, st>>>(d_blob, d_offs, idx_b.p, n, d_start.p, d_byte_base.p, P, fp.p, cmp.p, sig.p, ids.p, bytes.p); break;
         }
         CK(cudaGetLastError());
+        // pre-check off: equal (zero) signatures pass every pair through
+        if (!g_sig_precheck) CK(cudaMemsetAsync(sig.p, 0, n * sizeof(uint32_t), st));
         return launches + 1;
     }
 
@@ -479,7 +481,6 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
     P.w_fp = W.cmp.p;
     P.q_sig = Q.sig.p;
     P.w_sig = W.sig.p;
-    P.sig_thr = g_sig_precheck ? 2 * o.k : 64;
     P.w_bytes = W.bytes.p;
     P.w_ids = W.ids.p;
     P.id_base = D->id_base + sh.base;

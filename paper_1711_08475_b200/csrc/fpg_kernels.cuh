@@ -61,7 +61,6 @@ struct ScanParams {
     int32_t fold;               // field width for the generic fold (kGeneric only)
     const uint32_t* q_sig;      // occurrence signatures (verifier pre-check)
     const uint32_t* w_sig;
-    int32_t sig_thr;            // 2k, or 64 to disable the pre-check
 };
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
@@ -124,8 +123,8 @@ __device__ __forceinline__ uint64_t onehot_count16(uint64_t fp) {
 }
 
 // Occurrence signature of a string: bit (c & 31) for every byte c.  One edit
-// changes at most two of its bits, so popc(sig_a ^ sig_b) > 2k proves
-// distance > k for Hamming and Levenshtein alike (the occurrence bound of
+// changes at most two of its bits, so popc(sig_a ^ sig_b) > 2 proves
+// distance > 1 (hence > k for k <= 1) for Hamming and Levenshtein alike (the occurrence bound of
 // fingerprint.hpp:216-224 over a 32-letter hashed alphabet).  K2's verifier
 // uses it as an exact pre-check before comparing bytes.
 __device__ __forceinline__ uint32_t occurrence_sig(const uint8_t* s, int n) {

@@ -180,13 +180,10 @@ __device__ __forceinline__ T lds_t(uint32_t a) {
     }
 }
 
-// popc(x) <= t for t in {0, 2} without the XU pipe (clear the lowest set bit twice).
-__device__ __forceinline__ bool popc_le(uint32_t x, int t) {
-    if (t >= 32) return true;
-    if (t == 0) return x == 0;
+// popc(x) <= 2 without the XU pipe (clear the lowest set bit twice).
+__device__ __forceinline__ bool popc_le2(uint32_t x) {
     const uint32_t y = x & (x - 1);
-    if (t == 1) return y == 0;
-    return (y & (y - 1)) == 0 || t > 2;
+    return (y & (y - 1)) == 0;
 }
 
 // Per-tile state of one warp (all members live in registers once inlined).
@@ -275,7 +272,7 @@ struct TileScan {
                                              const uint32_t (&wg)[kWordsPerLane],
                                              const bool (&wv)[kWordsPerLane], uint32_t a_wsurv) {
         const T mf = (T)P.mask_fold, ms = (T)P.mask_single;
-        const int thr = P.thr, sthr = P.sig_thr;
+        const int thr = P.thr;
         unsigned total = 0;
         for (uint32_t j = 0; j < tl.q_count; j += 2) {
             const bool two = j + 1 < tl.q_count;
@@ -292,11 +289,11 @@ struct TileScan {
                 if constexpr (!FULL) { f0 &= wv[r]; f1 &= wv[r]; }
                 bool s0, s1;
                 if (r < 5) {
-                    s0 = __popc(g0 ^ wg[r]) <= sthr;
-                    s1 = __popc(g1 ^ wg[r]) <= sthr;
+                    s0 = __popc(g0 ^ wg[r]) <= 2;
+                    s1 = __popc(g1 ^ wg[r]) <= 2;
                 } else {
-                    s0 = popc_le(g0 ^ wg[r], sthr);
-                    s1 = popc_le(g1 ^ wg[r], sthr);
+                    s0 = popc_le2(g0 ^ wg[r]);
+                    s1 = popc_le2(g1 ^ wg[r]);
                 }
                 mfp |= (f0 ? (1u << r) : 0u) | (f1 ? (0x100u << r) : 0u);
                 mboth |= ((f0 & s0) ? (1u << r) : 0u) | ((f1 & s1) ? (0x100u << r) : 0u);
