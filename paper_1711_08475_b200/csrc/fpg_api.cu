@@ -376,12 +376,15 @@ void for_each_shard(size_t n, F&& f) {
 template <int KIND, int W, bool STATS>
 void launch_scan(const fpg::Tile* tiles, uint32_t ntiles, const fpg::ScanParams& P, cudaStream_t st,
                  int device) {
+    auto kern = fpg::k_scan<KIND, W, STATS>;
+    constexpr size_t smem = fpg::scan_smem_bytes(W, STATS);
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fpg::k_scan<KIND, W, STATS>, fpg::kScanThreads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, fpg::kScanThreads, smem));
     const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)sms * std::max(per_sm, 1) * 8);
-    fpg::k_scan<KIND, W, STATS><<<(unsigned)std::max<uint64_t>(grid, 1), fpg::kScanThreads, 0, st>>>(tiles, ntiles, P);
+    kern<<<(unsigned)std::max<uint64_t>(grid, 1), fpg::kScanThreads, smem, st>>>(tiles, ntiles, P);
     CK(cudaGetLastError());
 }
 

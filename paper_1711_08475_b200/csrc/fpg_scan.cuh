@@ -155,7 +155,7 @@ constexpr int kScanWarps = kScanThreads / 32;
 constexpr int kWordsPerLane = 8;                                   // R
 constexpr int kTileWords = kScanThreads * kWordsPerLane;           // 2048
 constexpr int kTileQueries = 256;
-constexpr int kLaneCap = 24;                                       // queue slots per lane
+constexpr int kLaneCap = 16;                                       // queue slots per lane
 
 // 32-bit shared-window addressing (keeps generic->shared conversions out of loops).
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -186,6 +186,33 @@ __device__ __forceinline__ bool popc_le2(uint32_t x) {
     return (y & (y - 1)) == 0;
 }
 
+// Pass flags of 4 fingerprint distances at once: d_t (<= 64) packed into byte t,
+// byte + (127 - thr) carries into bit 7 exactly when d_t > thr (no byte overflows
+// since 64 + 127 < 256).  Returns bit 8t+7 set iff d_t <= thr.
+__device__ __forceinline__ uint32_t pass_flags4(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t d3,
+                                                uint32_t bias) {
+    const uint32_t packed = d0 + d1 * 0x100u + d2 * 0x10000u + d3 * 0x1000000u;
+    return ~(packed + bias) & 0x80808080u;
+}
+
+// Queue entry / mask layout.  An iteration compares queries j, j+1 (qi = 0, 1)
+// with the lane's words r = 4h + t (h, t in 0..3 x 0..1).  Flag register
+// k = 2 qi + h holds word t at bit 8t+7; the four registers are merged as
+// f0 | f1 >> 1 | f2 >> 2 | f3 >> 3 (bit 8t+7-k) and compressed to 16 bits:
+// mask bit i <-> t = i >> 2, k = 3 - (i & 3).
+__device__ __forceinline__ uint32_t merge_flags(uint32_t f0, uint32_t f1, uint32_t f2, uint32_t f3) {
+    return f0 | (f1 >> 1) | (f2 >> 2) | (f3 >> 3);
+}
+__device__ __forceinline__ uint32_t compress16(uint32_t m) {  // bits 4..7 of each byte -> 16 bits
+    const uint32_t z = (m >> 4) | (m >> 8);
+    return __byte_perm(z, 0, 0x4420);                          // bytes 0, 2 of z
+}
+__device__ __forceinline__ void decode_bit(int i, uint32_t& qi, uint32_t& r) {
+    const int t = i >> 2, k = 3 - (i & 3);
+    qi = (uint32_t)(k >> 1);
+    r = (uint32_t)(4 * (k & 1) + t);
+}
+
 // Per-tile state of one warp (all members live in registers once inlined).
 template <int KIND, typename T, bool STATS>
 struct TileScan {
@@ -195,7 +222,7 @@ struct TileScan {
     const uint8_t* wbytes;
     int m, n, qs, ws, vclass, tid, lane;
     uint32_t a_queue;    // shared address of this lane's queue slot 0 (slot s at + 128 s)
-    uint32_t a_qlimit;   // flush once the next push could pass the last slot
+    uint32_t a_qlimit;   // flush once qp passes the last slot
     uint32_t a_qsig;
     uint32_t qp;
 
@@ -217,9 +244,9 @@ struct TileScan {
         return verify_pair(qb, m, qs, wb, n, ws, P.k);
     }
 
-    // Verifies every queued entry of the warp by byte compares.  Entry =
-    // (j << 16) | mask(j+1) << 8 | mask(j): pairs of queries j, j+1 with this
-    // lane's 8 words that passed both the fingerprint and the signature test.
+    // Byte-verifies every queued entry of the warp.  Entry = (j << 16) | m16:
+    // the pairs of queries j, j+1 with this lane's words that passed both the
+    // fingerprint and the signature test (rare: each lane walks its own bits).
     __device__ __forceinline__ void flush() {
         __syncwarp();
         const uint32_t lt_mask = (1u << lane) - 1u;
@@ -234,10 +261,12 @@ struct TileScan {
                 bool hit = false;
                 uint32_t j = 0, widx = 0;
                 if (keep) {
-                    const int b = 31 - __clz(keep);
-                    keep ^= 1u << b;
-                    j = j0 + (b >> 3);
-                    widx = (uint32_t)((b & 7) * kScanThreads + tid);
+                    const int i = 31 - __clz(keep);
+                    keep ^= 1u << i;
+                    uint32_t qi, r;
+                    decode_bit(i, qi, r);
+                    j = j0 + qi;
+                    widx = r * kScanThreads + (uint32_t)tid;
                     hit = verify_bytes(j, widx);
                 }
                 const uint32_t hb = __ballot_sync(0xffffffffu, hit);
@@ -260,19 +289,21 @@ struct TileScan {
         qp = a_queue;
     }
 
-    // Filter loop over the tile's queries, two per iteration.  Per pair: the
-    // reference fingerprint test (counted for QueryStats) and the exact
-    // occurrence-signature test; pairs passing both are queued.  The
-    // signature popcount runs on the XU pipe for words 0..4 and as ALU
-    // bit-clears for words 5..7, balancing the two pipes.  FULL: all 8 words
-    // of every lane are valid (all but each bucket's last tile).  Returns the
-    // warp's fingerprint-survivor count (STATS only).
-    template <bool FULL>
+    // Filter loop over the tile's queries, two per iteration (16 pairs per
+    // lane).  Per pair: the reference fingerprint test (its survivors are the
+    // QueryStats::verified count) and the exact occurrence-signature test
+    // (popc(sig_q ^ sig_w) <= 2); both results as packed-byte flags, 4 pairs
+    // per register.  Signature popcounts of words 0..5 run on the XU pipe,
+    // words 6..7 as ALU bit-clears, balancing the two pipes.  Pairs passing
+    // both tests are queued as one (j, 16-bit mask) entry.  vmask clears
+    // invalid words (a bucket's last tile).  Returns the warp's fingerprint
+    // survivor count (STATS only).
     __device__ __forceinline__ unsigned scan(uint32_t a_q, const T (&wc)[kWordsPerLane],
-                                             const uint32_t (&wg)[kWordsPerLane],
-                                             const bool (&wv)[kWordsPerLane], uint32_t a_wsurv) {
+                                             const uint32_t (&wg)[kWordsPerLane], uint32_t vmask,
+                                             uint32_t a_wsurv) {
         const T mf = (T)P.mask_fold, ms = (T)P.mask_single;
-        const int thr = P.thr;
+        const uint32_t bias = (uint32_t)(127 - min(P.thr, 127)) * 0x01010101u;
+        constexpr uint32_t sbias = 125u * 0x01010101u;  // signature: popc <= 2 passes
         unsigned total = 0;
         for (uint32_t j = 0; j < tl.q_count; j += 2) {
             const bool two = j + 1 < tl.q_count;
@@ -281,28 +312,36 @@ struct TileScan {
             const T q1 = lds_t<T>(a_q + (uint32_t)sizeof(T) * j1);
             const uint32_t g0 = lds32(a_qsig + 4u * j);
             const uint32_t g1 = lds32(a_qsig + 4u * j1);
-            uint32_t mfp = 0, mboth = 0;
+            uint32_t d[2][kWordsPerLane], s[2][kWordsPerLane];
 #pragma unroll
             for (int r = 0; r < kWordsPerLane; ++r) {
-                bool f0 = distance_of<KIND, T>(q0 ^ wc[r], mf, ms, P.fold) <= thr;
-                bool f1 = distance_of<KIND, T>(q1 ^ wc[r], mf, ms, P.fold) <= thr;
-                if constexpr (!FULL) { f0 &= wv[r]; f1 &= wv[r]; }
-                bool s0, s1;
-                if (r < 5) {
-                    s0 = __popc(g0 ^ wg[r]) <= 2;
-                    s1 = __popc(g1 ^ wg[r]) <= 2;
+                d[0][r] = (uint32_t)distance_of<KIND, T>(q0 ^ wc[r], mf, ms, P.fold);
+                d[1][r] = (uint32_t)distance_of<KIND, T>(q1 ^ wc[r], mf, ms, P.fold);
+                if (r < 6) {
+                    s[0][r] = (uint32_t)__popc(g0 ^ wg[r]);
+                    s[1][r] = (uint32_t)__popc(g1 ^ wg[r]);
                 } else {
-                    s0 = popc_le2(g0 ^ wg[r]);
-                    s1 = popc_le2(g1 ^ wg[r]);
+                    s[0][r] = popc_le2(g0 ^ wg[r]) ? 0u : 3u;
+                    s[1][r] = popc_le2(g1 ^ wg[r]) ? 0u : 3u;
                 }
-                mfp |= (f0 ? (1u << r) : 0u) | (f1 ? (0x100u << r) : 0u);
-                mboth |= ((f0 & s0) ? (1u << r) : 0u) | ((f1 & s1) ? (0x100u << r) : 0u);
             }
-            if (!two) { mfp &= 0xffu; mboth &= 0xffu; }
-            sts32(qp, (j << 16) | mboth);  // unconditional: the slot is free until qp moves
-            qp += mboth ? 128u : 0u;
+            const uint32_t f0 = pass_flags4(d[0][0], d[0][1], d[0][2], d[0][3], bias);
+            const uint32_t f1 = pass_flags4(d[0][4], d[0][5], d[0][6], d[0][7], bias);
+            const uint32_t f2 = pass_flags4(d[1][0], d[1][1], d[1][2], d[1][3], bias);
+            const uint32_t f3 = pass_flags4(d[1][4], d[1][5], d[1][6], d[1][7], bias);
+            const uint32_t t0 = pass_flags4(s[0][0], s[0][1], s[0][2], s[0][3], sbias);
+            const uint32_t t1 = pass_flags4(s[0][4], s[0][5], s[0][6], s[0][7], sbias);
+            const uint32_t t2 = pass_flags4(s[1][0], s[1][1], s[1][2], s[1][3], sbias);
+            const uint32_t t3 = pass_flags4(s[1][4], s[1][5], s[1][6], s[1][7], sbias);
+            uint32_t vm = vmask;
+            if (!two) vm &= 0xC0C0C0C0u;  // keep qi = 0 (k = 0, 1 -> bits 7, 6)
+            const uint32_t both = merge_flags(f0 & t0, f1 & t1, f2 & t2, f3 & t3) & vm;
+            sts32(qp, __byte_perm(compress16(both), j, 0x5410));  // unconditional: slot free until qp moves
+            qp += both ? 128u : 0u;
             if constexpr (STATS) {
-                const unsigned c = __reduce_add_sync(0xffffffffu, (unsigned)(__popc(mfp & 0xffu) | (__popc(mfp >> 8) << 16)));
+                const uint32_t fp = merge_flags(f0, f1, f2, f3) & vm;
+                const unsigned c = __reduce_add_sync(
+                    0xffffffffu, (unsigned)(__popc(fp & 0xC0C0C0C0u) | (__popc(fp & 0x30303030u) << 16)));
                 if (lane == 0) {
                     sts32(a_wsurv + 4u * j, c & 0xffffu);
                     if (two) sts32(a_wsurv + 4u * j1, c >> 16);
@@ -320,15 +359,16 @@ template <int KIND, int W, bool STATS>
 __global__ void __launch_bounds__(kScanThreads, 4) k_scan(const Tile* __restrict__ tiles, uint32_t ntiles,
                                                           const __grid_constant__ ScanParams P) {
     using T = typename std::conditional<(W <= 32), uint32_t, uint64_t>::type;
-    __shared__ T s_q[kTileQueries];
-    __shared__ uint32_t s_qsig[kTileQueries];
-    __shared__ uint32_t s_wsurv[STATS ? kScanWarps : 1][STATS ? kTileQueries : 1];
-    __shared__ uint32_t s_queue[kScanWarps * kLaneCap * 32];
+    extern __shared__ __align__(16) uint8_t smem[];
+    // dynamic shared memory carve-up
+    T* s_q = reinterpret_cast<T*>(smem);                                          // kTileQueries
+    uint32_t* s_qsig = reinterpret_cast<uint32_t*>(s_q + kTileQueries);           // kTileQueries
+    uint32_t* s_wsurv = s_qsig + kTileQueries;                                    // warps x kTileQueries (STATS)
+    uint32_t* s_queue = s_wsurv + (STATS ? kScanWarps * kTileQueries : 0);        // warps x cap x 32
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // lane-private queue, slot-major: slot s of this lane at word (warp*cap + s)*32 + lane
     const uint32_t a_queue = smem_u32(s_queue) + 4u * (uint32_t)(warp * kLaneCap * 32 + lane);
     const uint32_t a_q = smem_u32(s_q), a_qsig = smem_u32(s_qsig);
-    const uint32_t a_wsurv = smem_u32(s_wsurv[STATS ? warp : 0]);
+    const uint32_t a_wsurv = smem_u32(s_wsurv + (STATS ? warp * kTileQueries : 0));
     unsigned long long surv_warp = 0;  // lane 0's copy is the warp total (STATS)
 
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -340,13 +380,15 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(const Tile* __restrict
         }
         T wc[kWordsPerLane];
         uint32_t wg[kWordsPerLane];
-        bool wv[kWordsPerLane];
+        uint32_t vmask = 0;
 #pragma unroll
         for (int r = 0; r < kWordsPerLane; ++r) {
             const uint32_t widx = r * kScanThreads + tid;
-            wv[r] = widx < tl.w_count;
-            wc[r] = wv[r] ? (T)P.w_fp[tl.w_begin + widx] : (T)0;
-            wg[r] = wv[r] ? P.w_sig[tl.w_begin + widx] : 0u;
+            const bool ok = widx < tl.w_count;
+            wc[r] = ok ? (T)P.w_fp[tl.w_begin + widx] : (T)0;
+            wg[r] = ok ? P.w_sig[tl.w_begin + widx] : 0u;
+            // flag bits of word r = 4h + t for both queries: bit 8t + 7 - k, k = 2 qi + h
+            if (ok) vmask |= (1u << (8 * (r & 3) + 7 - (r >> 2))) | (1u << (8 * (r & 3) + 5 - (r >> 2)));
         }
         __syncthreads();
 
@@ -355,8 +397,7 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(const Tile* __restrict
                                         tl.q_len, tl.w_len, tl.q_stride, tl.w_stride,
                                         (tl.q_len <= 16 && tl.w_len <= 16) ? 1 : (tl.q_len <= 32 && tl.w_len <= 32) ? 2 : 0,
                                         tid, lane, a_queue, a_queue + 128u * (kLaneCap - 1), a_qsig, a_queue};
-            surv_warp += (tl.w_count == kTileWords) ? ts.template scan<true>(a_q, wc, wg, wv, a_wsurv)
-                                                    : ts.template scan<false>(a_q, wc, wg, wv, a_wsurv);
+            surv_warp += ts.scan(a_q, wc, wg, vmask, a_wsurv);
         } else if constexpr (STATS) {
             // incompatible lengths with the length prefilter off: the reference
             // still runs the fingerprint test (dictionary.hpp:102-106) and
@@ -367,9 +408,10 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(const Tile* __restrict
                 unsigned c = 0;
 #pragma unroll
                 for (int r = 0; r < kWordsPerLane; ++r)
-                    c += ((distance_of<KIND, T>(qc ^ wc[r], mf, ms, P.fold) <= P.thr) & wv[r]) ? 1u : 0u;
+                    c += ((distance_of<KIND, T>(qc ^ wc[r], mf, ms, P.fold) <= P.thr) &&
+                          (r * kScanThreads + tid < (int)tl.w_count)) ? 1u : 0u;
                 c = __reduce_add_sync(0xffffffffu, c);
-                if (lane == 0) s_wsurv[warp][j] = c;
+                if (lane == 0) s_wsurv[warp * kTileQueries + j] = c;
                 surv_warp += c;
             }
         }
@@ -378,13 +420,19 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(const Tile* __restrict
             for (uint32_t i = tid; i < tl.q_count; i += kScanThreads) {
                 uint32_t v = 0;
 #pragma unroll
-                for (int w = 0; w < kScanWarps; ++w) v += s_wsurv[w][i];
+                for (int w = 0; w < kScanWarps; ++w) v += s_wsurv[w * kTileQueries + i];
                 if (v) atomicAdd(&P.q_survivors[P.q_ids[tl.q_begin + i]], v);
             }
         }
     }
     // run total of fingerprint survivors (reported), one atomic per warp
     if (STATS && lane == 0 && surv_warp) atomicAdd(P.survivors_total, surv_warp);
+}
+
+// Dynamic shared memory of k_scan<.., W, STATS>.
+__host__ __device__ constexpr size_t scan_smem_bytes(int W, bool stats) {
+    return (size_t)kTileQueries * (W <= 32 ? 4 : 8) + 4u * kTileQueries +
+           (stats ? 4u * kScanWarps * kTileQueries : 0) + 4u * kScanWarps * kLaneCap * 32;
 }
 
 }  // namespace fpg

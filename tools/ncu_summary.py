@@ -1,0 +1,87 @@
+#!/usr/bin/env python
+"""Summarise ncu outputs for profiles/: a launch list (--metrics
+gpu__time_duration.sum --csv) and/or a --set full report of one kernel.
+
+usage: tools/ncu_summary.py launches <launches.csv>
+       tools/ncu_summary.py report <prof.ncu-rep> [<src-lines>]
+"""
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+RAW_KEYS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed.sum", "launch__registers_per_thread", "launch__grid_size",
+    "launch__block_size", "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
+    "sm__cycles_elapsed.avg.per_second",
+]
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hdr = None
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for r in rows:
+        if "Kernel Name" in r:
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            d = dict(zip(hdr, r))
+            if d.get("Metric Name") == "gpu__time_duration.sum":
+                unit = d.get("Metric Unit", "ns")
+                v = float(d["Metric Value"].replace(",", ""))
+                v *= {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "nsecond": 1e-3, "ms": 1e3, "msecond": 1e3}.get(unit, 1e-3)
+                k = d["Kernel Name"].split("(")[0][:90]
+                agg[k][0] += 1
+                agg[k][1] += v
+    tot = sum(v[1] for v in agg.values())
+    print(f"{'launches':>8} {'total us':>10} {'avg us':>9} {'share':>6}  kernel")
+    for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print(f"{v[0]:8d} {v[1]:10.1f} {v[1] / v[0]:9.1f} {100 * v[1] / tot:5.1f}%  {k}")
+    print(f"total device time of listed launches: {tot:.1f} us (serialised, cold-cache; compare shares)")
+
+
+def report(path, nlines=25):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    d = dict(zip(hdr, vals))
+    u = dict(zip(hdr, units))
+    print("kernel:", d.get("Kernel Name", "?"))
+    for k in RAW_KEYS:
+        if k in d:
+            print(f"  {k} = {d[k]} {u.get(k, '')}")
+    src = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                         capture_output=True, text=True).stdout
+    out, fname = [], None
+    for r in csv.reader(io.StringIO(src)):
+        if len(r) >= 2 and r[0] == "File Path":
+            fname = r[1].split("/")[-1]
+        if r and r[0] and r[0].isdigit() and len(r) > 7:
+            def num(x):
+                try:
+                    return int(x)
+                except ValueError:
+                    return 0
+            out.append((num(r[7]), num(r[4]), fname, int(r[0]), r[1].strip()[:80]))
+    ti = sum(o[0] for o in out) or 1
+    ts = sum(o[1] for o in out) or 1
+    print(f"  warp instructions executed: {ti}; stall samples: {ts}")
+    print("  top source lines by stall samples (instr share / sample share):")
+    for o in sorted(out, key=lambda x: -x[1])[:nlines]:
+        print(f"    {100 * o[0] / ti:5.1f}% {100 * o[1] / ts:5.1f}%  {o[2]}:{o[3]}  {o[4]}")
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "launches":
+        launches(sys.argv[2])
+    else:
+        report(sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 25)
