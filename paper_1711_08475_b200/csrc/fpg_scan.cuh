@@ -293,8 +293,8 @@ struct TileScan {
     // lane).  Per pair: the reference fingerprint test (its survivors are the
     // QueryStats::verified count) and the exact occurrence-signature test
     // (popc(sig_q ^ sig_w) <= 2); both results as packed-byte flags, 4 pairs
-    // per register.  Signature popcounts of words 0..5 run on the XU pipe,
-    // words 6..7 as ALU bit-clears, balancing the two pipes.  Pairs passing
+    // per register.  Signature popcounts of words 0..3 run on the XU pipe,
+    // words 4..7 as ALU bit-clears, balancing the two pipes.  Pairs passing
     // both tests are queued as one (j, 16-bit mask) entry.  vmask clears
     // invalid words (a bucket's last tile).  Returns the warp's fingerprint
     // survivor count (STATS only).
@@ -317,7 +317,7 @@ struct TileScan {
             for (int r = 0; r < kWordsPerLane; ++r) {
                 d[0][r] = (uint32_t)distance_of<KIND, T>(q0 ^ wc[r], mf, ms, P.fold);
                 d[1][r] = (uint32_t)distance_of<KIND, T>(q1 ^ wc[r], mf, ms, P.fold);
-                if (r < 6) {
+                if (r < 4) {
                     s[0][r] = (uint32_t)__popc(g0 ^ wg[r]);
                     s[1][r] = (uint32_t)__popc(g1 ^ wg[r]);
                 } else {
