@@ -30,7 +30,6 @@ import json
 import math
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -47,7 +46,7 @@ POPC_PER_CLK_PER_SM = 16  # measured: tools/microbench/intpipe.cu (profiles/r01_
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=2)
@@ -59,47 +58,54 @@ def parse():
 
 
 class Clocks:
-    """nvidia-smi sampling of SM clocks / throttle reasons during the timed region."""
+    """NVML sampling (every 10 ms, background thread) of SM clocks and clock
+    event (throttle) reasons, kept only while the timed region is open."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index: int):
-        self.index, self.samples, self.proc = index, [], None
+        self.index, self.samples, self.active, self.stop_flag = index, [], False, False
+        self.max_mhz, self.err = None, None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        except Exception as e:  # no NVML: report it, never guess
+            self.nv, self.err = None, f"nvml unavailable: {e}"
+
+    def _loop(self):
+        while not self.stop_flag:
+            if self.active:
+                try:
+                    sm = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                    rs = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    self.samples.append((float(sm), int(rs)))
+                except Exception as e:
+                    self.err = str(e)
+            time.sleep(0.01)
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+        if self.nv:
+            self.t = threading.Thread(target=self._loop, daemon=True)
             self.t.start()
-        except FileNotFoundError:
-            self.proc = None
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
-                self.samples.append(parts)
+    def open(self):
+        self.active = True
+
+    def close(self):
+        self.active = False
 
     def stop(self) -> dict:
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self.stop_flag = True
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": float(self.samples[0][1]) if self.samples[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [self.err or "no samples"]}
+        reasons = sorted({name for _, r in self.samples for bit, name in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples), "source": "nvml, 10 ms"}
 
 
 def dist_env():
@@ -260,6 +266,7 @@ def main():
     clocks.start()
     run_ms, filt_ms, launches, executed, survivors = [], [], 0, 0, 0
     barrier()
+    clocks.open()
     for _ in range(args.steps):
         if flush is not None:
             flush.zero_()  # L2 flush (256 MB > 126 MB L2), outside the event-timed run
@@ -271,6 +278,7 @@ def main():
         launches += t["launches"]
         executed, survivors = t["executed_pairs"], t["survivors"]
     barrier()
+    clocks.close()
     clk = clocks.stop()
     csr, st = batch.download()
     total_ms = reduce_max(sum(run_ms), world)

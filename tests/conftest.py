@@ -35,3 +35,21 @@ def reference():
     if not Reference.available():
         pytest.skip("oracle/_ref not built (reference tree absent when building)")
     return Reference()
+
+
+def build_api_check(tmp_dir: Path) -> Path:
+    """Compiles tests/cpp/api_check.cpp against include/fingerprints/b200.hpp
+    and links libfpg.so (the C++ drop-in surface)."""
+    import shutil
+    import subprocess
+
+    from paper_1711_08475_b200._lib import LIBFPG
+
+    cxx = shutil.which("g++")
+    if not cxx:
+        pytest.skip("g++ not available")
+    exe = tmp_dir / "api_check"
+    subprocess.run([cxx, "-std=c++20", "-O1", "-Wall", "-Werror", f"-I{ROOT / 'include'}",
+                    str(ROOT / "tests" / "cpp" / "api_check.cpp"), f"-L{LIBFPG.parent}", "-lfpg",
+                    f"-Wl,-rpath,{LIBFPG.parent}", "-o", str(exe)], check=True)
+    return exe

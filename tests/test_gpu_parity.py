@@ -247,3 +247,18 @@ def test_config2_full_dictionary_subsample(oracle):
     with GpuFingerprintedDictionary((blob, offs), s, devices=(0, 0)) as d2:
         c2, _ = d2.query_batch((qblob, qoffs), opt)
     assert np.array_equal(csr.word_ids, c2.word_ids)
+
+
+@pytest.mark.gpu
+def test_cpp_drop_in_queries(tmp_path):
+    """The C++ FingerprintedDictionary alias (b200.hpp) answers query /
+    query_batch like a brute-force scan and throws invalid_argument for
+    position + Levenshtein, as dictionary.hpp:78-79 does."""
+    import subprocess
+
+    from conftest import build_api_check
+
+    exe = build_api_check(tmp_path)
+    out = subprocess.run([str(exe), "gpu"], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr + out.stdout
+    assert "api_check gpu: ok" in out.stdout

@@ -182,3 +182,15 @@ def test_product_never_imports_the_oracle():
     for path in (ROOT / "paper_1711_08475_b200" / "csrc").rglob("*"):
         if path.is_file():
             assert "fp_oracle" not in path.read_text(errors="ignore"), path
+
+
+def test_cpp_drop_in_headers_compile_and_host_logic(tmp_path):
+    """Reference-style C++ caller code compiles against include/fingerprints/
+    and its host-side logic (Scheme, LetterSet, render, errors) holds."""
+    import subprocess
+
+    from conftest import build_api_check
+
+    exe = build_api_check(tmp_path)
+    out = subprocess.run([str(exe), "host"], capture_output=True, text=True, check=True).stdout
+    assert "api_check host: ok" in out
