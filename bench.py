@@ -264,7 +264,7 @@ def main():
         batch.run(opt, want_stats=True)
     clocks = Clocks(dev)
     clocks.start()
-    run_ms, filt_ms, launches, executed, survivors = [], [], 0, 0, 0
+    run_ms, filt_ms, launches, executed, survivors, candidates = [], [], 0, 0, 0, 0
     barrier()
     clocks.open()
     for _ in range(args.steps):
@@ -276,7 +276,7 @@ def main():
         run_ms.append(t["run_ms"])
         filt_ms.append(t["filter_ms"])
         launches += t["launches"]
-        executed, survivors = t["executed_pairs"], t["survivors"]
+        executed, survivors, candidates = t["executed_pairs"], t["survivors"], t["candidates"]
     barrier()
     clocks.close()
     clk = clocks.stop()
@@ -325,6 +325,7 @@ def main():
                    "parallelism": f"dict-shard x{world}"},
         "queries_per_s": nq * args.steps / (total_ms / 1e3),
         "executed_pairs_per_step": executed, "survivors_per_step": survivors,
+        "verifier_candidates_per_step": candidates,
         "matches_per_step": int(csr.offsets[-1]),
         "construction_s": build_s,
         "gpu_launches": launches,

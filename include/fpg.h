@@ -144,6 +144,10 @@ int fpg_batch_last_timing(const fpg_batch* batch, int32_t shard, double* run_ms,
                           double* filter_ms, uint64_t* executed_pairs, uint64_t* survivors,
                           uint64_t* kernel_launches);
 
+/* Pairs of the last run on `shard` that reached the byte verifier (after
+ * the fingerprint test and the verifier's own exact pre-filters). */
+int fpg_batch_last_candidates(const fpg_batch* batch, int32_t shard, uint64_t* candidates);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,6 +23,7 @@
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "../../include/fpg.h"
 #include "fpg_kernels.cuh"
@@ -62,6 +63,8 @@ int guarded(F&& f) {
 }
 
 inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+// per-run device counters: out_count, survivors, tile counter, candidates, big segment flag
+constexpr int kNumCounters = 5;
 inline int stride_of(int len) { return len <= 16 ? 16 : (len + 15) & ~15; }
 
 // Device buffer that grows on demand (never shrinks), freed on destruction.
@@ -121,7 +124,7 @@ struct HBuf {
 fpg::SchemeParams make_params(const fpg_scheme& s) {
     fpg::SchemeParams P;
     std::memset(&P, 0, sizeof(P));
-    for (int c = 0; c < 256; ++c) P.slot[c] = -1;
+    for (int c = 0; c < 256; ++c) P.slot[c] = P.sigbit[c] = -1;
     for (int i = 0; i < s.nletters; ++i) P.slot[s.letters[i]] = (int8_t)i;
     P.variant = s.variant;
     P.width = s.width;
@@ -184,6 +187,8 @@ const bool g_sig_precheck = [] {
     return !(e && e[0] == '0');
 }();
 
+enum BuildMode { kGenericDict = 0, kSliceDict = 1, kSliceQuery = 2 };
+
 // Strings of one collection, length-bucketed on one device.
 struct Collection {
     uint64_t n = 0;
@@ -192,13 +197,20 @@ struct Collection {
     uint64_t total_bytes = 0;
     int max_len = 0;
     DBuf<uint64_t> fp;   // reference-layout fingerprints (prints())
-    DBuf<uint64_t> cmp;  // comparison words K2 reads (== fp, or the one-hot count-16 form)
-    DBuf<uint32_t> sig;  // occurrence signatures (verifier pre-check)
+    DBuf<uint64_t> cmp;  // generic K2: comparison words (== fp, or the one-hot count-16 form)
+    DBuf<uint32_t> sig;  // generic K2: occurrence signatures (verifier pre-check)
+    DBuf<uint32_t> sigp; // bit-sliced K2: sig' codes (fpg_slice.cuh)
     DBuf<uint32_t> ids;
     DBuf<uint8_t> bytes;
     DBuf<uint32_t> d_start;
     DBuf<uint64_t> d_byte_base;
-    // scratch
+    // bit-sliced dictionary: per length slab ranges and plane offsets
+    std::vector<uint32_t> slab_start;    // L1 + 1
+    std::vector<uint64_t> plane_base;    // L1
+    DBuf<uint32_t> planes;
+    DBuf<uint32_t> d_slab_start, d_count;
+    DBuf<uint64_t> d_plane_base;
+    // scratch (len_b = lengths in sorted order; kept for query collections)
     DBuf<uint16_t> len_a, len_b;
     DBuf<uint32_t> idx_a, idx_b;
     DBuf<uint32_t> hist;
@@ -208,7 +220,7 @@ struct Collection {
     // Builds the bucketed layout of n strings already on the device.
     // Returns the number of kernel launches issued (ours, not CUB's).
     uint64_t build(const uint8_t* d_blob, const uint64_t* d_offs, uint64_t n_, const fpg::SchemeParams& P,
-                   cudaStream_t st) {
+                   cudaStream_t st, BuildMode mode, int npt) {
         n = n_;
         const int L1 = fpg::kMaxLen + 1;
         count.assign(L1, 0);
@@ -219,11 +231,16 @@ struct Collection {
         h_hist.reserve(L1 + 1);
         CK(cudaMemsetAsync(hist.p, 0, sizeof(uint32_t) * (L1 + 1), st));
         fp.reserve(n);
-        cmp.reserve(n);
-        sig.reserve(n);
+        if (mode == kGenericDict) {
+            cmp.reserve(n);
+            sig.reserve(n);
+        } else {
+            sigp.reserve(n);
+        }
         ids.reserve(n);
+        len_b.reserve(n);
         if (n) {
-            len_a.reserve(n); len_b.reserve(n); idx_a.reserve(n); idx_b.reserve(n);
+            len_a.reserve(n); idx_a.reserve(n); idx_b.reserve(n);
             fpg::k_lengths<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(d_offs, n, len_a.p, idx_a.p, hist.p,
                                                                    hist.p + L1);
             CK(cudaGetLastError());
@@ -258,20 +275,87 @@ struct Collection {
         CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, tmp, len_a.p, len_b.p, idx_a.p, idx_b.p, (int)n, 0,
                                            end_bit, st));
         const unsigned grid = (unsigned)cdiv(n, 256);
+        uint64_t* cmp_p = mode == kGenericDict ? cmp.p : nullptr;
+        uint32_t* sig_p = mode == kGenericDict ? sig.p : nullptr;
+        uint32_t* sigp_p = mode == kGenericDict ? nullptr : sigp.p;
+#define FPG_BUILD(V) fpg::k_build<V><<<grid, 256, 0, st>>>(d_blob, d_offs, idx_b.p, n, d_start.p, d_byte_base.p, P, \
+                                                           fp.p, cmp_p, sig_p, sigp_p, ids.p, bytes.p)
         switch (P.variant) {
-            case 0: fpg::k_build<0><<<grid, 256, 0, st>>>(d_blob, d_offs, idx_b.p, n, d_start.p, d_byte_base.p, P, fp.p, cmp.p, sig.p, ids.p, bytes.p); break;
-            case 1: fpg::k_build<1><<<grid, 256, 0, st>>>(d_blob, d_offs, idx_b.p, n, d_start.p, d_byte_base.p, P, fp.p, cmp.p, sig.p, ids.p, bytes.p); break;
-            case 2: fpg::k_build<2><<<grid, 256, 0, st>>>(d_blob, d_offs, idx_b.p, n, d_start.p, d_byte_base.p, P, fp.p, cmp.p, sig.p, ids.p, bytes.p); break;
-            default: fpg::k_build<3><<<grid, 256, 0, st>>>(d_blob, d_offs, idx_b.p, n, d_start.p, d_byte_base.p, P, fp.p, cmp.p, sig.p, ids.p, bytes.p); break;
+            case 0: FPG_BUILD(0); break;
+            case 1: FPG_BUILD(1); break;
+            case 2: FPG_BUILD(2); break;
+            default: FPG_BUILD(3); break;
         }
+#undef FPG_BUILD
         CK(cudaGetLastError());
+        ++launches;
         // pre-check off: equal (zero) signatures pass every pair through
-        if (!g_sig_precheck) CK(cudaMemsetAsync(sig.p, 0, n * sizeof(uint32_t), st));
-        return launches + 1;
+        if (mode == kGenericDict && !g_sig_precheck) CK(cudaMemsetAsync(sig.p, 0, n * sizeof(uint32_t), st));
+        if (mode == kSliceDict) {
+            slab_start.assign(L1 + 1, 0);
+            plane_base.assign(L1, 0);
+            uint64_t sl = 0, pb = 0;
+            for (int L = 0; L < L1; ++L) {
+                slab_start[L] = (uint32_t)sl;
+                plane_base[L] = pb;
+                const uint64_t ns = cdiv(count[L], 32);
+                sl += ns;
+                pb += ns * (uint64_t)npt;
+            }
+            slab_start[L1] = (uint32_t)sl;
+            planes.reserve(pb);
+            d_slab_start.reserve(L1 + 1);
+            d_count.reserve(L1);
+            d_plane_base.reserve(L1);
+            CK(cudaMemcpyAsync(d_slab_start.p, slab_start.data(), sizeof(uint32_t) * (L1 + 1), cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(d_count.p, count.data(), sizeof(uint32_t) * L1, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(d_plane_base.p, plane_base.data(), sizeof(uint64_t) * L1, cudaMemcpyHostToDevice, st));
+            fpg::k_planes<<<(unsigned)cdiv(sl * 32, 256), 256, 0, st>>>(fp.p, sigp.p, d_slab_start.p, d_start.p,
+                                                                        d_count.p, d_plane_base.p, L1, (uint32_t)sl,
+                                                                        P.width, npt, planes.p);
+            CK(cudaGetLastError());
+            ++launches;
+        }
+        return launches;
     }
 
     void drop_scratch() {
         len_a.release(); len_b.release(); idx_a.release(); idx_b.release(); cub_tmp.release();
+    }
+
+    // Query collection whose length order and bucket tables were built on the
+    // host at upload (counting sort, fpg_batch_upload): one K1 launch, which
+    // also zeroes the per-query survivor counts and the run counters.
+    uint64_t build_sorted(const uint8_t* d_blob, const uint64_t* d_offs, const uint32_t* d_order,
+                          const fpg::SchemeParams& P, cudaStream_t st, BuildMode mode, uint32_t* zero_by_id,
+                          unsigned long long* zero64, int nzero64) {
+        fp.reserve(n);
+        if (mode == kGenericDict) {
+            cmp.reserve(n);
+            sig.reserve(n);
+        } else {
+            sigp.reserve(n);
+        }
+        ids.reserve(n);
+        len_b.reserve(n);
+        bytes.reserve(total_bytes);
+        uint64_t* cmp_p = mode == kGenericDict ? cmp.p : nullptr;
+        uint32_t* sig_p = mode == kGenericDict ? sig.p : nullptr;
+        uint32_t* sigp_p = mode == kGenericDict ? nullptr : sigp.p;
+        const unsigned grid = (unsigned)std::max<uint64_t>(1, cdiv(n, 256));
+#define FPG_BUILD(V) fpg::k_build<V><<<grid, 256, 0, st>>>(d_blob, d_offs, d_order, n, d_start.p, d_byte_base.p, P, \
+                                                           fp.p, cmp_p, sig_p, sigp_p, ids.p, bytes.p, len_b.p,  \
+                                                           zero_by_id, zero64, nzero64)
+        switch (P.variant) {
+            case 0: FPG_BUILD(0); break;
+            case 1: FPG_BUILD(1); break;
+            case 2: FPG_BUILD(2); break;
+            default: FPG_BUILD(3); break;
+        }
+#undef FPG_BUILD
+        CK(cudaGetLastError());
+        if (mode == kGenericDict && !g_sig_precheck && n) CK(cudaMemsetAsync(sig.p, 0, n * sizeof(uint32_t), st));
+        return 1;
     }
 };
 
@@ -280,6 +364,10 @@ struct Shard {
     cudaStream_t stream = nullptr;
     uint64_t base = 0, n = 0;  // input index range [base, base + n)
     Collection dict;
+    DBuf<uint8_t> blob;        // construction staging
+    DBuf<uint64_t> offs;
+    DBuf<unsigned long long> d_hist;
+    HBuf<unsigned long long> h_hist;
 };
 
 }  // namespace
@@ -287,6 +375,8 @@ struct Shard {
 struct fpg_dict {
     fpg_scheme scheme;
     fpg::SchemeParams params;
+    bool slice = false;     // bit-sliced K2 (fpg_slice.cuh); else the generic k_scan
+    int npt = 0;            // planes per slab: W + sig' fields
     uint64_t n = 0, id_base = 0;
     std::vector<std::unique_ptr<Shard>> shards;
     std::vector<uint64_t> len_count;  // whole-dictionary bucket counts (all shards)
@@ -302,10 +392,12 @@ struct ShardBatch {
     Shard* sh = nullptr;
     DBuf<uint8_t> qblob;
     DBuf<uint64_t> qoffs;
+    DBuf<uint32_t> qorder;
     Collection queries;
     DBuf<fpg::Tile> tiles;
+    DBuf<fpg::SliceTile> stiles;
     DBuf<unsigned long long> out, sorted;
-    DBuf<unsigned long long> counters;  // [0] out_count, [1] survivors_total
+    DBuf<unsigned long long> counters;  // [0] out_count, [1] survivors_total, [2] tile counter
     DBuf<uint32_t> qsurv;
     DBuf<uint64_t> offsets;
     DBuf<uint32_t> ids;
@@ -314,7 +406,7 @@ struct ShardBatch {
     HBuf<uint64_t> h_offsets;
     HBuf<uint32_t> h_ids, h_qsurv;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-    uint64_t total = 0, executed = 0, survivors = 0, launches = 0;
+    uint64_t total = 0, executed = 0, survivors = 0, candidates = 0, launches = 0;
     double run_ms = 0, filter_ms = 0;
     uint64_t out_cap = 1 << 20;
 };
@@ -325,6 +417,13 @@ struct fpg_batch {
     fpg_dict* dict = nullptr;
     uint64_t nq = 0;
     std::vector<uint32_t> qlen;  // host copy of query lengths (stats bookkeeping)
+    // length buckets of the queries (host counting sort at upload)
+    std::vector<uint32_t> qcount, qstart;
+    std::vector<uint64_t> qbbase;
+    int qmax_len = 0;
+    uint64_t qtotal_bytes = 0;
+    HBuf<uint32_t> h_order, h_start;
+    HBuf<uint64_t> h_bbase;
     std::vector<std::unique_ptr<ShardBatch>> sb;
     fpg_query_options opt{};
     bool ran = false;
@@ -419,6 +518,63 @@ void dispatch_scan(const fpg::SchemeParams& S, bool stats, const fpg::Tile* tile
     }
 }
 
+template <int NP, int FW, int EXTRA, int S>
+void launch_slice(const fpg::SliceTile* tiles, uint32_t ntiles, const fpg::SliceParams& P, cudaStream_t st,
+                  int device) {
+    auto kern = fpg::k_slice<NP, FW, EXTRA, S>;
+    constexpr size_t smem = fpg::slice_smem_bytes(NP + S);
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, fpg::kSliceThreads, smem));
+    const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)sms * std::max(per_sm, 1));
+    kern<<<(unsigned)std::max<uint64_t>(grid, 1), fpg::kSliceThreads, smem, st>>>(tiles, ntiles, P);
+    CK(cudaGetLastError());
+}
+
+template <int NP, int FW, int EXTRA>
+void launch_slice_s(int nsig, const fpg::SliceTile* tiles, uint32_t ntiles, const fpg::SliceParams& P,
+                    cudaStream_t st, int device) {
+    switch (nsig) {
+        case 0: launch_slice<NP, FW, EXTRA, 0>(tiles, ntiles, P, st, device); break;
+        case 8: launch_slice<NP, FW, EXTRA, 8>(tiles, ntiles, P, st, device); break;
+        case 12: launch_slice<NP, FW, EXTRA, 12>(tiles, ntiles, P, st, device); break;
+        default: launch_slice<NP, FW, EXTRA, 16>(tiles, ntiles, P, st, device); break;
+    }
+}
+
+// Field width of the scheme's multi-bit fields (1 for occurrence / halved).
+int field_width_of(const fpg_scheme& s) {
+    if (s.variant == FPG_COUNT) return s.bits_per_count;
+    if (s.variant == FPG_POSITION) return s.bits_per_position;
+    return 1;
+}
+
+bool slice_supported(const fpg_scheme& s) {
+    const int fw = field_width_of(s);
+    return fw >= 1 && fw <= 4;
+}
+
+template <int NP>
+void dispatch_slice_w(int fw, int nsig, const fpg::SliceTile* tiles, uint32_t ntiles, const fpg::SliceParams& P,
+                      cudaStream_t st, int device) {
+    switch (fw) {
+        case 1: launch_slice_s<NP, 1, 0>(nsig, tiles, ntiles, P, st, device); break;
+        case 2: launch_slice_s<NP, 2, 0>(nsig, tiles, ntiles, P, st, device); break;
+        case 3: launch_slice_s<NP, 3, NP % 3>(nsig, tiles, ntiles, P, st, device); break;
+        default: launch_slice_s<NP, 4, 0>(nsig, tiles, ntiles, P, st, device); break;
+    }
+}
+
+void dispatch_slice(const fpg_scheme& sc, int nsig, const fpg::SliceTile* tiles, uint32_t ntiles,
+                    const fpg::SliceParams& P, cudaStream_t st, int device) {
+    const int fw = field_width_of(sc);
+    if (sc.width == 16) dispatch_slice_w<16>(fw, nsig, tiles, ntiles, P, st, device);
+    else if (sc.width == 32) dispatch_slice_w<32>(fw, nsig, tiles, ntiles, P, st, device);
+    else dispatch_slice_w<64>(fw, nsig, tiles, ntiles, P, st, device);
+}
+
 bool compatible(int metric, int k, int lq, int lw) {
     if (metric == FPG_HAMMING) return lq == lw;
     return std::abs(lq - lw) <= k;
@@ -435,107 +591,221 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
     CK(cudaEventRecord(S.ev[0], st));
     const uint64_t nq = B->nq;
     // K1 on the queries (pattern fingerprint inside query time, dictionary.hpp:84)
-    S.launches += S.queries.build(S.qblob.p, S.qoffs.p, nq, D->params, st);
+    S.qsurv.reserve(2 * nq);  // [0, nq): fingerprint survivors, [nq, 2 nq): matches
+    S.counters.reserve(kNumCounters);
+    S.h_counters.reserve(kNumCounters);
+    S.launches += S.queries.build_sorted(S.qblob.p, S.qoffs.p, S.qorder.p, D->params, st,
+                                         D->slice ? kSliceQuery : kGenericDict, S.qsurv.p, S.counters.p,
+                                         kNumCounters);
     const Collection& Q = S.queries;
     const Collection& W = sh.dict;
-
-    // Tile plan over compatible (query length, word length) bucket pairs.
     const bool count_only_pass = o.want_stats && o.use_filter && o.metric == FPG_LEVENSHTEIN && !o.length_prefilter;
-    std::vector<fpg::Tile> plan;
     uint64_t executed = 0;
-    for (int lq = 0; lq <= Q.max_len; ++lq) {
-        if (!Q.count[lq]) continue;
+    std::vector<fpg::Tile> plan;
+    std::vector<fpg::SliceTile> splan;
+
+    if (D->slice) {
+        // Tile plan: per word length lw, the compatible query lengths form one
+        // contiguous range of the length-sorted queries (Hamming / k = 0:
+        // lw; Levenshtein k = 1: lw - 1 .. lw + 1, edit_distance.hpp:38-39).
+        // Tiles = (<= 256 SL slabs) x (<= kSliceQ queries), largest first,
+        // handed out by an atomic counter.
+        const uint32_t chunk = fpg::kSliceThreads * fpg::slice_slabs_per_lane(D->npt);
+        const int L1 = fpg::kMaxLen + 1;
+        // query chunk: the largest of 128 / 64 / 32 that still gives every
+        // resident CTA (2 per SM) about 8 tiles, so the dynamic schedule ends evenly
+        uint64_t units = 0;  // (query, slab-chunk) units of the verified ranges
         for (int lw = 0; lw <= W.max_len; ++lw) {
             if (!W.count[lw]) continue;
-            const bool comp = compatible(o.metric, o.k, lq, lw);
-            if (!comp && !count_only_pass) continue;
-            if (comp) executed += (uint64_t)Q.count[lq] * W.count[lw];
-            for (uint32_t q0 = 0; q0 < Q.count[lq]; q0 += fpg::kTileQueries) {
-                for (uint32_t w0 = 0; w0 < W.count[lw]; w0 += fpg::kTileWords) {
-                    fpg::Tile t{};
-                    t.q_begin = Q.start[lq] + q0;
-                    t.q_count = std::min<uint32_t>(fpg::kTileQueries, Q.count[lq] - q0);
-                    t.w_begin = W.start[lw] + w0;
-                    t.w_count = std::min<uint32_t>(fpg::kTileWords, W.count[lw] - w0);
-                    t.q_bytes = Q.byte_base[lq] + (uint64_t)q0 * stride_of(lq);
-                    t.w_bytes = W.byte_base[lw] + (uint64_t)w0 * stride_of(lw);
-                    t.q_len = (uint16_t)lq;
+            const int span = (o.metric == FPG_HAMMING) ? 0 : o.k;
+            const int lo = std::max(0, lw - span), hi = std::min(L1 - 1, lw + span);
+            units += (uint64_t)(Q.start[hi] + Q.count[hi] - Q.start[lo]) * cdiv(cdiv(W.count[lw], 32), chunk);
+        }
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, sh.device);
+        uint32_t qchunk = fpg::kSliceQ;
+        while (qchunk > 32 && units / qchunk < (uint64_t)sms * 2 * 8) qchunk >>= 1;
+        auto add = [&](int lw, uint32_t qb, uint32_t qe, bool count_only) {
+            const uint32_t ns = (uint32_t)cdiv(W.count[lw], 32);
+            for (uint32_t q0 = qb; q0 < qe; q0 += qchunk)
+                for (uint32_t s0 = 0; s0 < ns; s0 += chunk) {
+                    fpg::SliceTile t{};
+                    t.slab_begin = s0;
+                    t.n_slabs = std::min(chunk, ns - s0);
+                    t.q_begin = q0;
+                    t.q_count = std::min<uint32_t>(qchunk, qe - q0);
+                    t.plane_base = W.plane_base[lw];
+                    t.w_bytes = W.byte_base[lw];
+                    t.ns = ns;
+                    t.w_start = W.start[lw];
+                    t.w_count = W.count[lw];
                     t.w_len = (uint16_t)lw;
-                    t.q_stride = (uint16_t)stride_of(lq);
                     t.w_stride = (uint16_t)stride_of(lw);
-                    t.count_only = comp ? 0u : 1u;
-                    plan.push_back(t);
+                    t.count_only = count_only ? 1u : 0u;
+                    splan.push_back(t);
+                }
+        };
+        for (int lw = 0; lw <= W.max_len; ++lw) {
+            if (!W.count[lw]) continue;
+            const int span = (o.metric == FPG_HAMMING) ? 0 : o.k;
+            const int lo = std::max(0, lw - span), hi = std::min(L1 - 1, lw + span);
+            const uint32_t qb = Q.start[lo], qe = Q.start[hi] + Q.count[hi];
+            executed += (uint64_t)(qe - qb) * W.count[lw];
+            add(lw, qb, qe, false);
+            if (count_only_pass) {
+                add(lw, 0, qb, true);
+                add(lw, qe, (uint32_t)nq, true);
+            }
+        }
+        std::stable_sort(splan.begin(), splan.end(), [](const fpg::SliceTile& x, const fpg::SliceTile& y) {
+            return (uint64_t)x.q_count * x.n_slabs > (uint64_t)y.q_count * y.n_slabs;
+        });
+        S.stiles.reserve(splan.size());
+        if (!splan.empty())
+            CK(cudaMemcpyAsync(S.stiles.p, splan.data(), splan.size() * sizeof(fpg::SliceTile),
+                               cudaMemcpyHostToDevice, st));
+    } else {
+        // Generic k_scan: one tile per (query length, word length) bucket pair block.
+        for (int lq = 0; lq <= Q.max_len; ++lq) {
+            if (!Q.count[lq]) continue;
+            for (int lw = 0; lw <= W.max_len; ++lw) {
+                if (!W.count[lw]) continue;
+                const bool comp = compatible(o.metric, o.k, lq, lw);
+                if (!comp && !count_only_pass) continue;
+                if (comp) executed += (uint64_t)Q.count[lq] * W.count[lw];
+                for (uint32_t q0 = 0; q0 < Q.count[lq]; q0 += fpg::kTileQueries) {
+                    for (uint32_t w0 = 0; w0 < W.count[lw]; w0 += fpg::kTileWords) {
+                        fpg::Tile t{};
+                        t.q_begin = Q.start[lq] + q0;
+                        t.q_count = std::min<uint32_t>(fpg::kTileQueries, Q.count[lq] - q0);
+                        t.w_begin = W.start[lw] + w0;
+                        t.w_count = std::min<uint32_t>(fpg::kTileWords, W.count[lw] - w0);
+                        t.q_bytes = Q.byte_base[lq] + (uint64_t)q0 * stride_of(lq);
+                        t.w_bytes = W.byte_base[lw] + (uint64_t)w0 * stride_of(lw);
+                        t.q_len = (uint16_t)lq;
+                        t.w_len = (uint16_t)lw;
+                        t.q_stride = (uint16_t)stride_of(lq);
+                        t.w_stride = (uint16_t)stride_of(lw);
+                        t.count_only = comp ? 0u : 1u;
+                        plan.push_back(t);
+                    }
                 }
             }
         }
+        S.tiles.reserve(plan.size());
+        if (!plan.empty())
+            CK(cudaMemcpyAsync(S.tiles.p, plan.data(), plan.size() * sizeof(fpg::Tile), cudaMemcpyHostToDevice, st));
     }
     S.executed = executed;
-    S.tiles.reserve(plan.size());
-    if (!plan.empty())
-        CK(cudaMemcpyAsync(S.tiles.p, plan.data(), plan.size() * sizeof(fpg::Tile), cudaMemcpyHostToDevice, st));
 
-    S.qsurv.reserve(nq);
-    S.counters.reserve(2);
-    S.h_counters.reserve(2);
     fpg::ScanParams P{};
-    P.q_fp = Q.cmp.p;
-    P.q_bytes = Q.bytes.p;
-    P.q_ids = Q.ids.p;
-    P.w_fp = W.cmp.p;
-    P.q_sig = Q.sig.p;
-    P.w_sig = W.sig.p;
-    P.w_bytes = W.bytes.p;
-    P.w_ids = W.ids.p;
-    P.id_base = D->id_base + sh.base;
-    P.q_survivors = S.qsurv.p;
-    P.out_count = S.counters.p;
-    P.survivors_total = S.counters.p + 1;
-    P.mask_fold = D->params.mask_fold;
-    P.mask_single = D->params.mask_single;
-    // reject iff F_D > 2k (ceil_half(F_D) > k, dictionary.hpp:102-106); the
-    // one-hot count form counts every differing field twice
-    P.thr = o.use_filter ? (D->params.onehot ? 4 * o.k : 2 * o.k) : 1 << 20;
-    P.k = o.k;
-    P.fold = D->params.variant == FPG_COUNT ? D->params.b
-           : D->params.variant == FPG_POSITION ? D->params.p : 1;
-    for (;;) {
+    fpg::SliceParams SP{};
+    if (D->slice) {
+        SP.planes = W.planes.p;
+        SP.q_fp = Q.fp.p;
+        SP.q_sigp = Q.sigp.p;
+        SP.q_len = Q.len_b.p;
+        SP.q_start = Q.d_start.p;
+        SP.q_bbase = Q.d_byte_base.p;
+        SP.q_bytes = Q.bytes.p;
+        SP.q_ids = Q.ids.p;
+        SP.w_bytes = W.bytes.p;
+        SP.w_ids = W.ids.p;
+        SP.id_base = D->id_base + sh.base;
+        SP.q_survivors = S.qsurv.p;
+        SP.out_count = S.counters.p;
+        SP.survivors_total = S.counters.p + 1;
+        SP.tile_counter = reinterpret_cast<unsigned int*>(S.counters.p + 2);
+        SP.candidates = S.counters.p + 3;
+        SP.q_matches = S.qsurv.p + nq;
+        SP.big_seg = S.counters.p + 4;
+        SP.k = o.k;
+        SP.stats = (o.want_stats && o.use_filter) ? 1 : 0;
+        SP.use_fp = supports(D->scheme.variant, o.metric) ? 1 : 0;
+    } else {
+        P.q_fp = Q.cmp.p;
+        P.q_bytes = Q.bytes.p;
+        P.q_ids = Q.ids.p;
+        P.w_fp = W.cmp.p;
+        P.q_sig = Q.sig.p;
+        P.w_sig = W.sig.p;
+        P.w_bytes = W.bytes.p;
+        P.w_ids = W.ids.p;
+        P.id_base = D->id_base + sh.base;
+        P.q_survivors = S.qsurv.p;
+        P.out_count = S.counters.p;
+        P.survivors_total = S.counters.p + 1;
+        P.mask_fold = D->params.mask_fold;
+        P.mask_single = D->params.mask_single;
+        // reject iff F_D > 2k (ceil_half(F_D) > k, dictionary.hpp:102-106); the
+        // one-hot count form counts every differing field twice
+        P.thr = o.use_filter ? (D->params.onehot ? 4 * o.k : 2 * o.k) : 1 << 20;
+        P.k = o.k;
+        P.fold = D->params.variant == FPG_COUNT ? D->params.b
+               : D->params.variant == FPG_POSITION ? D->params.p : 1;
+        P.q_matches = S.qsurv.p + nq;
+        P.big_seg = S.counters.p + 4;
+    }
+    for (bool first = true;; first = false) {
         S.out.reserve(S.out_cap);
-        P.out = S.out.p;
-        P.out_cap = S.out.cap;
-        CK(cudaMemsetAsync(S.counters.p, 0, 2 * sizeof(unsigned long long), st));
-        if (nq) CK(cudaMemsetAsync(S.qsurv.p, 0, nq * sizeof(uint32_t), st));
+        P.out = SP.out = S.out.p;
+        P.out_cap = SP.out_cap = S.out.cap;
+        if (!first) {  // rescan after growing the output (K1 zeroed them the first time)
+            CK(cudaMemsetAsync(S.counters.p, 0, kNumCounters * sizeof(unsigned long long), st));
+            if (nq) CK(cudaMemsetAsync(S.qsurv.p, 0, 2 * nq * sizeof(uint32_t), st));
+        }
         CK(cudaEventRecord(S.ev[1], st));
-        if (!plan.empty()) {
+        if (D->slice && !splan.empty()) {
+            dispatch_slice(D->scheme, D->params.nsig, S.stiles.p, (uint32_t)splan.size(), SP, st, sh.device);
+            ++S.launches;
+        } else if (!D->slice && !plan.empty()) {
             dispatch_scan(D->params, o.want_stats != 0, S.tiles.p, (uint32_t)plan.size(), P, st, sh.device);
             ++S.launches;
         }
         CK(cudaEventRecord(S.ev[2], st));
-        CK(cudaMemcpyAsync(S.h_counters.p, S.counters.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(S.h_counters.p, S.counters.p, kNumCounters * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         if (S.h_counters.p[0] <= S.out.cap) break;
         S.out_cap = S.h_counters.p[0] + S.h_counters.p[0] / 4 + 1024;  // grow and rescan
     }
     S.total = S.h_counters.p[0];
     S.survivors = S.h_counters.p[1];
+    S.candidates = S.h_counters.p[3];
 
     // K4: order (query, word) keys and build the CSR.
     S.sorted.reserve(S.total);
     S.offsets.reserve(nq + 1);
     S.ids.reserve(S.total);
-    if (S.total) {
-        int end_bit = 33;
-        while (end_bit < 64 && (1ull << (end_bit - 32)) <= nq) ++end_bit;
+    int end_bit = 33;
+    while (end_bit < 64 && (1ull << (end_bit - 32)) <= nq) ++end_bit;
+    if (S.total && !S.h_counters.p[4]) {
+        // every query has <= kSegMax matches: offsets = exclusive scan of the
+        // per-query counts, keys scattered into their segments, one warp
+        // sorts each segment (no global sort, no further host round trip)
+        size_t tmp = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, S.qsurv.p + nq, S.offsets.p, (int)nq, st));
+        S.cub_tmp.reserve(tmp);
+        CK(cub::DeviceScan::ExclusiveSum(S.cub_tmp.p, tmp, S.qsurv.p + nq, S.offsets.p, (int)nq, st));
+        fpg::k_seg_scatter<<<(unsigned)cdiv(S.total, 256), 256, 0, st>>>(S.out.p, S.counters.p, S.offsets.p,
+                                                                         S.qsurv.p + nq, nq, S.ids.p,
+                                                                         S.offsets.p + nq);
+        CK(cudaGetLastError());
+        fpg::k_seg_sort<<<(unsigned)cdiv(nq * 32, 256), 256, 0, st>>>(S.offsets.p, nq, S.ids.p);
+        CK(cudaGetLastError());
+        S.launches += 2;
+    } else if (!S.total) {
+        CK(cudaMemsetAsync(S.offsets.p, 0, (nq + 1) * sizeof(uint64_t), st));
+    } else {
         size_t tmp = 0;
         CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, S.out.p, S.sorted.p, (int)S.total, 0, end_bit, st));
         S.cub_tmp.reserve(tmp);
         CK(cub::DeviceRadixSort::SortKeys(S.cub_tmp.p, tmp, S.out.p, S.sorted.p, (int)S.total, 0, end_bit, st));
         fpg::k_low_ids<<<(unsigned)cdiv(S.total, 256), 256, 0, st>>>(S.sorted.p, S.total, S.ids.p);
         CK(cudaGetLastError());
-        ++S.launches;
+        fpg::k_offsets<<<(unsigned)cdiv(nq + 1, 256), 256, 0, st>>>(S.sorted.p, S.total, nq, S.offsets.p);
+        CK(cudaGetLastError());
+        S.launches += 2;
     }
-    fpg::k_offsets<<<(unsigned)cdiv(nq + 1, 256), 256, 0, st>>>(S.sorted.p, S.total, nq, S.offsets.p);
-    CK(cudaGetLastError());
-    ++S.launches;
     CK(cudaEventRecord(S.ev[3], st));
     CK(cudaEventSynchronize(S.ev[3]));
     float ms = 0;
@@ -575,30 +845,71 @@ void upload(fpg_batch* B, const uint8_t* qbytes, const uint64_t* qoffsets, uint6
     if (nq >= (1ull << 31)) throw Error(FPG_EINVAL, "too many queries in one batch");
     B->nq = nq;
     B->qlen.resize(nq);
+    const int L1 = fpg::kMaxLen + 1;
+    B->qcount.assign(L1, 0);
     const uint64_t q0 = nq ? qoffsets[0] : 0;
     for (uint64_t i = 0; i < nq; ++i) {
         if (qoffsets[i + 1] < qoffsets[i]) throw Error(FPG_EINVAL, "query offsets not ascending");
         const uint64_t len = qoffsets[i + 1] - qoffsets[i];
         if (len > (uint64_t)fpg::kMaxLen) throw Error(FPG_EINVAL, "query longer than FPG_MAX_WORD_LEN");
         B->qlen[i] = (uint32_t)len;
+        ++B->qcount[len];
+    }
+    if (nq && qoffsets[nq] > q0 && !qbytes) throw Error(FPG_EINVAL, "null query bytes");
+    // Length buckets: stable counting sort of the query ids (the layout K1
+    // writes, with the padded-byte offset of every bucket).
+    B->qstart.assign(L1, 0);
+    B->qbbase.assign(L1, 0);
+    B->h_start.reserve(L1);
+    B->h_bbase.reserve(L1);
+    B->h_order.reserve(nq);
+    uint64_t pos = 0, bpos = 0;
+    B->qmax_len = 0;
+    for (int L = 0; L < L1; ++L) {
+        B->qstart[L] = (uint32_t)pos;
+        B->qbbase[L] = bpos;
+        B->h_start.p[L] = (uint32_t)pos;
+        B->h_bbase.p[L] = bpos;
+        pos += B->qcount[L];
+        bpos += (uint64_t)B->qcount[L] * stride_of(L);
+        if (B->qcount[L]) B->qmax_len = L;
+    }
+    B->qtotal_bytes = bpos;
+    {
+        std::vector<uint32_t> cur(B->qstart);
+        for (uint64_t i = 0; i < nq; ++i) B->h_order.p[cur[B->qlen[i]]++] = (uint32_t)i;
     }
     const uint64_t nbytes = nq ? qoffsets[nq] - q0 : 0;
     for_each_shard(B->sb.size(), [&](size_t i) {
         ShardBatch& S = *B->sb[i];
         CK(cudaSetDevice(S.sh->device));
-        S.qblob.reserve(nbytes);
+        cudaStream_t st = S.sh->stream;
+        S.qblob.reserve(nbytes + 16);
         S.qoffs.reserve(nq + 1);
-        if (nbytes) CK(cudaMemcpyAsync(S.qblob.p, qbytes + q0, nbytes, cudaMemcpyHostToDevice, S.sh->stream));
+        S.qorder.reserve(nq);
+        Collection& Q = S.queries;
+        Q.n = nq;
+        Q.count = B->qcount;
+        Q.start = B->qstart;
+        Q.byte_base = B->qbbase;
+        Q.max_len = B->qmax_len;
+        Q.total_bytes = B->qtotal_bytes;
+        Q.d_start.reserve(L1);
+        Q.d_byte_base.reserve(L1);
+        if (nbytes) CK(cudaMemcpyAsync(S.qblob.p, qbytes + q0, nbytes, cudaMemcpyHostToDevice, st));
         if (nq) {
+            CK(cudaMemcpyAsync(S.qorder.p, B->h_order.p, nq * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
             if (q0 == 0) {
-                CK(cudaMemcpyAsync(S.qoffs.p, qoffsets, (nq + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, S.sh->stream));
+                CK(cudaMemcpyAsync(S.qoffs.p, qoffsets, (nq + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
             } else {
                 std::vector<uint64_t> rebased(nq + 1);
                 for (uint64_t j = 0; j <= nq; ++j) rebased[j] = qoffsets[j] - q0;
-                CK(cudaMemcpyAsync(S.qoffs.p, rebased.data(), (nq + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, S.sh->stream));
-                CK(cudaStreamSynchronize(S.sh->stream));
+                CK(cudaMemcpyAsync(S.qoffs.p, rebased.data(), (nq + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
             }
         }
+        CK(cudaMemcpyAsync(Q.d_start.p, B->h_start.p, L1 * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(Q.d_byte_base.p, B->h_bbase.p, L1 * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));  // caller buffers may be reused once upload returns
     });
 }
 
@@ -673,6 +984,27 @@ void download(fpg_batch* B, fpg_result* out) {
     }
 }
 
+// Chooses the K2 path and the sig' map: non-letter bytes of the dictionary,
+// ranked by frequency (descending, then byte), dealt round robin onto S
+// one-bit fields (S = 0 / 8 / 12 / 16 by how many such bytes exist; FPG_SIGP_BITS
+// overrides).  FPG_SLICE=0 selects the generic k_scan for A/B runs.
+void configure_slice(fpg_dict& D, const std::vector<unsigned long long>& hist) {
+    const char* e = std::getenv("FPG_SLICE");
+    D.slice = slice_supported(D.scheme) && !(e && e[0] == '0');
+    std::vector<int> others;
+    for (int c = 0; c < 256; ++c)
+        if (hist[c] && D.params.slot[c] < 0) others.push_back(c);
+    std::stable_sort(others.begin(), others.end(), [&](int a, int b) { return hist[a] > hist[b]; });
+    auto snap = [](size_t v) { return v == 0 ? 0 : v <= 8 ? 8 : v <= 12 ? 12 : 16; };
+    int S = snap(others.size());
+    if (const char* sb = std::getenv("FPG_SIGP_BITS")) S = snap((size_t)std::max(0, std::atoi(sb)));
+    std::memset(D.params.sigbit, -1, sizeof(D.params.sigbit));
+    if (S)
+        for (size_t r = 0; r < others.size(); ++r) D.params.sigbit[others[r]] = (int8_t)(r % S);
+    D.params.nsig = S;
+    D.npt = D.scheme.width + S;
+}
+
 void make_batch(fpg_dict* D, fpg_batch** out) {
     auto B = std::make_unique<fpg_batch>();
     B->dict = D;
@@ -744,23 +1076,45 @@ int fpg_dict_create(const uint8_t* bytes, const uint64_t* offsets, uint64_t n, c
             sh->n = n * (g + 1) / G - sh->base;
             D->shards.push_back(std::move(sh));
         }
+        // Phase 1: upload each shard's strings and count its bytes (sig' ranking).
         for_each_shard(G, [&](size_t g) {
             Shard& sh = *D->shards[g];
             CK(cudaSetDevice(sh.device));
             CK(cudaStreamCreateWithFlags(&sh.stream, cudaStreamNonBlocking));
             const uint64_t b0 = sh.n ? offsets[sh.base] : 0;
             const uint64_t nbytes = sh.n ? offsets[sh.base + sh.n] - b0 : 0;
-            DBuf<uint8_t> blob;
-            DBuf<uint64_t> offs;
-            blob.reserve(nbytes);
-            offs.reserve(sh.n + 1);
+            sh.blob.reserve(nbytes + 16);  // K1 reads whole aligned words past the end
+            sh.offs.reserve(sh.n + 1);
             std::vector<uint64_t> local(sh.n + 1);
             for (uint64_t i = 0; i <= sh.n; ++i) local[i] = (sh.n ? offsets[sh.base + i] : 0) - b0;
-            if (nbytes) CK(cudaMemcpyAsync(blob.p, bytes + b0, nbytes, cudaMemcpyHostToDevice, sh.stream));
-            CK(cudaMemcpyAsync(offs.p, local.data(), (sh.n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, sh.stream));
-            sh.dict.build(blob.p, offs.p, sh.n, D->params, sh.stream);
+            if (nbytes) CK(cudaMemcpyAsync(sh.blob.p, bytes + b0, nbytes, cudaMemcpyHostToDevice, sh.stream));
+            CK(cudaMemcpyAsync(sh.offs.p, local.data(), (sh.n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, sh.stream));
+            sh.d_hist.reserve(256);
+            sh.h_hist.reserve(256);
+            CK(cudaMemsetAsync(sh.d_hist.p, 0, 256 * sizeof(unsigned long long), sh.stream));
+            if (nbytes) {
+                fpg::k_hist256<<<(unsigned)std::min<uint64_t>(cdiv(nbytes, 256), 4096), 256, 0, sh.stream>>>(
+                    sh.blob.p, nbytes, sh.d_hist.p);
+                CK(cudaGetLastError());
+            }
+            CK(cudaMemcpyAsync(sh.h_hist.p, sh.d_hist.p, 256 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                               sh.stream));
+            CK(cudaStreamSynchronize(sh.stream));
+        });
+        std::vector<unsigned long long> hist(256, 0);
+        for (auto& sh : D->shards)
+            for (int c = 0; c < 256; ++c) hist[c] += sh->h_hist.p[c];
+        configure_slice(*D, hist);
+        // Phase 2: fingerprints, length buckets, padded bytes and (bit-sliced) planes.
+        for_each_shard(G, [&](size_t g) {
+            Shard& sh = *D->shards[g];
+            CK(cudaSetDevice(sh.device));
+            sh.dict.build(sh.blob.p, sh.offs.p, sh.n, D->params, sh.stream, D->slice ? kSliceDict : kGenericDict,
+                          D->npt);
             CK(cudaStreamSynchronize(sh.stream));
             sh.dict.drop_scratch();
+            sh.blob.release();
+            sh.offs.release();
         });
         for (auto& sh : D->shards)
             for (int L = 0; L <= fpg::kMaxLen; ++L) D->len_count[L] += sh->dict.count[L];
@@ -825,17 +1179,17 @@ int fpg_build_fingerprints(const uint8_t* bytes, const uint64_t* offsets, uint64
         std::unique_ptr<CUstream_st, void (*)(CUstream_st*)> guard(st, [](CUstream_st* s) { cudaStreamDestroy(s); });
         DBuf<uint8_t> blob;
         DBuf<uint64_t> offs, fp;
-        blob.reserve(nbytes);
+        blob.reserve(nbytes + 16);
         offs.reserve(n + 1);
         fp.reserve(n);
         if (nbytes) CK(cudaMemcpyAsync(blob.p, bytes + b0, nbytes, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(offs.p, local.data(), (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
         const unsigned grid = (unsigned)cdiv(n, 256);
         switch (P.variant) {
-            case 0: fpg::k_build<0><<<grid, 256, 0, st>>>(blob.p, offs.p, nullptr, n, nullptr, nullptr, P, fp.p, nullptr, nullptr, nullptr, nullptr); break;
-            case 1: fpg::k_build<1><<<grid, 256, 0, st>>>(blob.p, offs.p, nullptr, n, nullptr, nullptr, P, fp.p, nullptr, nullptr, nullptr, nullptr); break;
-            case 2: fpg::k_build<2><<<grid, 256, 0, st>>>(blob.p, offs.p, nullptr, n, nullptr, nullptr, P, fp.p, nullptr, nullptr, nullptr, nullptr); break;
-            default: fpg::k_build<3><<<grid, 256, 0, st>>>(blob.p, offs.p, nullptr, n, nullptr, nullptr, P, fp.p, nullptr, nullptr, nullptr, nullptr); break;
+            case 0: fpg::k_build<0><<<grid, 256, 0, st>>>(blob.p, offs.p, nullptr, n, nullptr, nullptr, P, fp.p, nullptr, nullptr, nullptr, nullptr, nullptr); break;
+            case 1: fpg::k_build<1><<<grid, 256, 0, st>>>(blob.p, offs.p, nullptr, n, nullptr, nullptr, P, fp.p, nullptr, nullptr, nullptr, nullptr, nullptr); break;
+            case 2: fpg::k_build<2><<<grid, 256, 0, st>>>(blob.p, offs.p, nullptr, n, nullptr, nullptr, P, fp.p, nullptr, nullptr, nullptr, nullptr, nullptr); break;
+            default: fpg::k_build<3><<<grid, 256, 0, st>>>(blob.p, offs.p, nullptr, n, nullptr, nullptr, P, fp.p, nullptr, nullptr, nullptr, nullptr, nullptr); break;
         }
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(out, fp.p, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
@@ -886,6 +1240,13 @@ int fpg_batch_last_timing(const fpg_batch* batch, int32_t shard, double* run_ms,
         if (executed_pairs) *executed_pairs = S.executed;
         if (survivors) *survivors = S.survivors;
         if (kernel_launches) *kernel_launches = S.launches;
+    });
+}
+
+int fpg_batch_last_candidates(const fpg_batch* batch, int32_t shard, uint64_t* candidates) {
+    return guarded([&] {
+        if (!batch || !candidates || shard < 0 || (size_t)shard >= batch->sb.size()) throw Error(FPG_EINVAL, "bad shard");
+        *candidates = batch->sb[(size_t)shard]->candidates;
     });
 }
 

@@ -24,6 +24,8 @@ constexpr int kMaxLen = 4096;
 // shared memory because lanes index it with divergent bytes.
 struct SchemeParams {
     int8_t slot[256];
+    int8_t sigbit[256];    // sig' field of a non-letter byte (fpg_slice.cuh), or -1
+    int32_t nsig;          // sig' fields S
     int32_t variant, width, b, p, nletters, slots, extra;
     int32_t onehot;        // count, W=16, b=2: K2 compares a 32-bit one-hot form
     uint64_t mask_fold;    // bit at the LSB of every multi-bit field (count / position)
@@ -61,54 +63,67 @@ struct ScanParams {
     int32_t fold;               // field width for the generic fold (kGeneric only)
     const uint32_t* q_sig;      // occurrence signatures (verifier pre-check)
     const uint32_t* w_sig;
+    uint32_t* q_matches;        // per input query: matches (K4 segment sizes)
+    unsigned long long* big_seg;  // set when a query exceeds kSegMax matches
 };
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
 // ---------------------------------------------------------------- K1 build
+// Incremental fingerprint builder: one call per letter occurrence (slot q of
+// byte i of an n-byte string), the reference builders generalised to W bits.
 template <int VARIANT>
-__device__ __forceinline__ uint64_t build_fp(const uint8_t* s, int n, const int8_t* slot,
-                                             const SchemeParams& P) {
-    const int W = P.width;
+struct FpBuilder {
     uint64_t bits = 0;
-    if (VARIANT == 0) {                                  // build_occurrence :216-224
-        for (int i = 0; i < n; ++i) {
-            int q = slot[s[i]];
-            if (q >= 0) bits |= 1ull << (W - 1 - q);
+    uint64_t seen = 0;  // position: letters already placed (<= 64 letters)
+
+    __device__ __forceinline__ void init(const SchemeParams& P) {
+        if (VARIANT == 3) {                              // build_position :258: every field starts absent
+            const uint64_t absent = (1ull << P.p) - 1;
+            for (int q = 0; q < P.slots; ++q) bits |= absent << (P.width - P.p * (q + 1));
         }
-    } else if (VARIANT == 1) {                           // build_occurrence_halved :226-238
-        const int half = n >> 1;
-        for (int i = 0; i < n; ++i) {
-            int q = slot[s[i]];
-            if (q >= 0) bits |= 1ull << (i < half ? W - 1 - 2 * q : W - 2 - 2 * q);
-        }
-    } else if (VARIANT == 2) {                           // build_count :240-254
-        const int b = P.b;
-        const uint64_t sat = (1ull << b) - 1;
-        for (int i = 0; i < n; ++i) {
-            int q = slot[s[i]];
-            if (q < 0) continue;
-            const int shift = W - b * (q + 1);
+    }
+    __device__ __forceinline__ void add(int q, int i, int n, const SchemeParams& P) {
+        const int W = P.width;
+        if (VARIANT == 0) {                              // build_occurrence :216-224
+            bits |= 1ull << (W - 1 - q);
+        } else if (VARIANT == 1) {                       // build_occurrence_halved :226-238 (half = n / 2)
+            bits |= 1ull << (i < (n >> 1) ? W - 1 - 2 * q : W - 2 - 2 * q);
+        } else if (VARIANT == 2) {                       // build_count :240-254 (saturating b-bit counter)
+            const uint64_t sat = (1ull << P.b) - 1;
+            const int shift = W - P.b * (q + 1);
             if (((bits >> shift) & sat) != sat) bits += 1ull << shift;
-        }
-    } else {                                             // build_position :256-274 (one pass)
-        const int p = P.p;
-        const uint64_t absent = (1ull << p) - 1;
-        uint64_t seen = 0;                               // letters already placed (<= 64)
-        for (int q = 0; q < P.slots; ++q) bits |= absent << (W - p * (q + 1));
-        for (int i = 0; i < n; ++i) {
-            int q = slot[s[i]];
-            if (q < 0 || ((seen >> q) & 1)) continue;
+        } else {                                         // build_position :256-274, one pass
+            if ((seen >> q) & 1) return;                 // first occurrence only
             seen |= 1ull << q;
             if (q < P.slots) {
-                const int shift = W - p * (q + 1);
+                const uint64_t absent = (1ull << P.p) - 1;
+                const int shift = W - P.p * (q + 1);
                 if ((uint64_t)i < absent) bits = (bits & ~(absent << shift)) | ((uint64_t)i << shift);
             } else {
                 bits |= 1ull << (P.extra - 1 - (q - P.slots));
             }
         }
     }
-    return bits;
+};
+
+// Bytes [at, at + rem) of `blob` (rem <= 16, zero beyond) as four little-endian
+// words: five independent aligned 4-byte loads and funnel shifts, so a string
+// costs one memory latency per 16 bytes.  Blobs carry >= 16 bytes of tail padding.
+__device__ __forceinline__ void load_chunk(const uint8_t* blob, uint64_t at, int rem, uint32_t (&w)[4]) {
+    const uint64_t base = at & ~3ull;
+    const uint32_t sh = (uint32_t)(at & 3) * 8;
+    const int need = (int)((at & 3) + rem + 3) >> 2;     // words overlapping the range
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(blob + base);
+    uint32_t v[5];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) v[j] = j < need ? __ldg(p + j) : 0u;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t x = __funnelshift_r(v[j], v[j + 1], sh);
+        const int keep = rem - 4 * j;                    // bytes of this word inside the string
+        w[j] = keep >= 4 ? x : keep <= 0 ? 0u : (x & ((1u << (8 * keep)) - 1u));
+    }
 }
 
 // Comparison form of a count-16 (b=2) fingerprint: field i (value v in 0..3)
@@ -120,17 +135,6 @@ __device__ __forceinline__ uint64_t onehot_count16(uint64_t fp) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) r |= 1u << (4 * i + (int)((fp >> (14 - 2 * i)) & 3u));
     return r;
-}
-
-// Occurrence signature of a string: bit (c & 31) for every byte c.  One edit
-// changes at most two of its bits, so popc(sig_a ^ sig_b) > 2 proves
-// distance > 1 (hence > k for k <= 1) for Hamming and Levenshtein alike (the occurrence bound of
-// fingerprint.hpp:216-224 over a 32-letter hashed alphabet).  K2's verifier
-// uses it as an exact pre-check before comparing bytes.
-__device__ __forceinline__ uint32_t occurrence_sig(const uint8_t* s, int n) {
-    uint32_t g = 0;
-    for (int i = 0; i < n; ++i) g |= 1u << (s[i] & 31);
-    return g;
 }
 
 // Inputs: raw blob + offsets, `order` = sorted position -> input index (stable
@@ -147,41 +151,55 @@ __global__ void __launch_bounds__(256) k_build(const uint8_t* __restrict__ blob,
                                                uint64_t* __restrict__ fp_out,
                                                uint64_t* __restrict__ cmp_out,
                                                uint32_t* __restrict__ sig_out,
+                                               uint32_t* __restrict__ sigp_out,
                                                uint32_t* __restrict__ id_out,
-                                               uint8_t* __restrict__ bytes_out) {
+                                               uint8_t* __restrict__ bytes_out,
+                                               uint16_t* __restrict__ len_out = nullptr,
+                                               uint32_t* __restrict__ zero_by_id = nullptr,
+                                               unsigned long long* __restrict__ zero64 = nullptr,
+                                               int nzero64 = 0) {
     __shared__ int8_t s_slot[256];
+    __shared__ int8_t s_sigbit[256];
     s_slot[threadIdx.x] = P.slot[threadIdx.x];           // blockDim == 256
+    s_sigbit[threadIdx.x] = P.sigbit[threadIdx.x];
     __syncthreads();
+    if (zero64 && blockIdx.x == 0 && (int)threadIdx.x < nzero64) zero64[threadIdx.x] = 0ull;
     const uint64_t pos = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (pos >= n) return;
     const uint32_t id = order ? order[pos] : (uint32_t)pos;
     const uint64_t beg = offsets[id];
     const int len = (int)(offsets[id + 1] - beg);
-    const uint8_t* s = blob + beg;
-    const uint64_t fp = build_fp<VARIANT>(s, len, s_slot, P);
-    fp_out[pos] = fp;
-    if (cmp_out) cmp_out[pos] = P.onehot ? onehot_count16(fp) : fp;
-    if (sig_out) sig_out[pos] = occurrence_sig(s, len);
-    if (id_out) id_out[pos] = id;
-    if (bytes_out) {
-        const int stride = len <= 16 ? 16 : (len + 15) & ~15;
-        uint8_t* dst = bytes_out + bucket_bytes[len] + (uint64_t)(pos - bucket_start[len]) * stride;
-        // dst is 16-byte aligned: assemble 16-byte chunks in registers.
-        for (int c = 0; c < stride; c += 16) {
-            uint32_t w[4];
+    if (len_out) len_out[pos] = (uint16_t)len;
+    if (zero_by_id) zero_by_id[id] = zero_by_id[id + n] = 0u;  // survivor and match counts
+    const int stride = len <= 16 ? 16 : (len + 15) & ~15;
+    uint8_t* dst = bytes_out ? bytes_out + bucket_bytes[len] + (uint64_t)(pos - bucket_start[len]) * stride : nullptr;
+    FpBuilder<VARIANT> fb;
+    fb.init(P);
+    uint32_t sig = 0, sigp = 0;
+    for (int c = 0; c < stride; c += 16) {
+        uint32_t w[4];
+        const int rem = min(16, len - c);
+        if (rem > 0) load_chunk(blob, beg + c, rem, w);
+        else w[0] = w[1] = w[2] = w[3] = 0u;
+        if (dst) *reinterpret_cast<uint4*>(dst + c) = make_uint4(w[0], w[1], w[2], w[3]);  // 16-byte aligned
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                uint32_t v = 0;
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const int i = c + 4 * j + t;
-                    if (i < len) v |= (uint32_t)s[i] << (8 * t);
-                }
-                w[j] = v;
+        for (int t = 0; t < 16; ++t) {
+            if (t < rem) {
+                const uint32_t byte = (w[t >> 2] >> (8 * (t & 3))) & 0xffu;
+                const int q = s_slot[byte];
+                if (q >= 0) fb.add(q, c + t, len, P);
+                sig |= 1u << (byte & 31);
+                const int g = s_sigbit[byte];
+                if (g >= 0) sigp |= 1u << g;
             }
-            *reinterpret_cast<uint4*>(dst + c) = make_uint4(w[0], w[1], w[2], w[3]);
         }
     }
+    const uint64_t fp = fb.bits;
+    fp_out[pos] = fp;
+    if (cmp_out) cmp_out[pos] = P.onehot ? onehot_count16(fp) : fp;
+    if (sig_out) sig_out[pos] = sig;
+    if (sigp_out) sigp_out[pos] = sigp;
+    if (id_out) id_out[pos] = id;
 }
 
 __global__ void k_lengths(const uint64_t* __restrict__ offsets, uint64_t n,
@@ -227,6 +245,51 @@ __global__ void k_low_ids(const unsigned long long* __restrict__ keys, uint64_t 
     if (i < total) ids[i] = (uint32_t)keys[i];
 }
 
+constexpr uint32_t kSegMax = 32;  // K4 warp-sorts segments up to this size
+
+// Match bookkeeping of one hit: per-query count (K4 segment size) and the
+// flag that routes K4 to the global radix sort when a segment is large.
+__device__ __forceinline__ void count_match(uint32_t* q_matches, unsigned long long* big_seg, uint32_t qid) {
+    if (atomicAdd(&q_matches[qid], 1u) == kSegMax) *big_seg = 1ull;
+}
+
+// K4 segmented (all segments <= kSegMax): keys -> their query's segment.
+__global__ void k_seg_scatter(const unsigned long long* __restrict__ keys, const unsigned long long* __restrict__ count,
+                              const uint64_t* __restrict__ offsets_in, uint32_t* __restrict__ cursor, uint64_t nq,
+                              uint32_t* __restrict__ ids, uint64_t* __restrict__ offsets_last) {
+    const uint64_t total = *count;
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) *offsets_last = total;
+    if (i >= total) return;
+    const unsigned long long k = keys[i];
+    const uint32_t q = (uint32_t)(k >> 32);
+    const uint32_t slot = atomicSub(&cursor[q], 1u) - 1u;
+    ids[offsets_in[q] + slot] = (uint32_t)k;
+}
+
+// One warp per query: bitonic sort of its <= 32 word ids in registers.
+__global__ void k_seg_sort(const uint64_t* __restrict__ offsets, uint64_t nq, uint32_t* __restrict__ ids) {
+    const uint64_t q = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (q >= nq) return;
+    const uint64_t o = offsets[q];
+    const int n = (int)(offsets[q + 1] - o);
+    if (n <= 1) return;
+    uint32_t v = lane < n ? ids[o + lane] : 0xffffffffu;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const uint32_t u = __shfl_xor_sync(0xffffffffu, v, j);
+            const bool up = (lane & k) == 0;
+            const bool lower = (lane & j) == 0;
+            v = (lower == up) ? min(v, u) : max(v, u);
+        }
+    }
+    if (lane < n) ids[o + lane] = v;
+}
+
 }  // namespace fpg
 
 #include "fpg_scan.cuh"
+#include "fpg_slice.cuh"

@@ -281,6 +281,7 @@ struct TileScan {
                             const uint64_t wid = P.id_base + P.w_ids[tl.w_begin + widx];
                             P.out[o] = (qid << 32) | wid;
                         }
+                        count_match(P.q_matches, P.big_seg, P.q_ids[tl.q_begin + j]);
                     }
                 }
             }

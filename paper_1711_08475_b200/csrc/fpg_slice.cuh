@@ -1,0 +1,411 @@
+// fpg_slice.cuh -- K2 as a bit-sliced scan (sm_100a): no POPC on the pair path.
+//
+// Layout.  The words of one dictionary length bucket are cut into slabs of 32
+// consecutive (input-ordered) words.  A slab is stored as NPT 32-bit planes:
+// plane b holds bit b of the 32 words' comparison codes (K1b k_planes).
+// Planes 0..NP-1 are the scheme fingerprint bits in the reference layout
+// (fingerprint.hpp:48-56, :138-147: NF fields of FW bits above EXTRA one-bit
+// fields); planes NP..NPT-1 are the "complement signature" sig' (below).
+// In HBM the planes of a bucket are plane-major: plane b of slab s at
+// plane_base + b * n_slabs + s, so lanes holding consecutive slabs load
+// coalesced 128-byte rows.
+//
+// Test.  The reference rejects a pair iff ceil(F_D / 2) > k, i.e. F_D > 2k
+// (dictionary.hpp:102-106, fingerprint.hpp:199,293-301), F_D = number of
+// fields whose bits differ (ComparisonTables, fingerprint.hpp:171-214).  Here
+// one lane evaluates it for the 32 words of a slab at once:
+//   x_b   = plane_b XOR query_bit_b         one IMAD: plane * s + m with
+//                                           (s, m) = (1, 0) or (-1, ~0), FMA pipe
+//   x_f   = OR of the field's x_b           (LOP3, fields wider than 1 bit)
+//   c2 |= c1 & x_f; c1 |= c0 & x_f; c0 |= x_f   three LOP3: saturating
+//                                           counters, c_i = "F >= i+1" per word
+// so bit w of c2 (c0 for k = 0) says word w is rejected.  Per 32 pairs that
+// is 3 ALU ops per 1-bit field (4 per wider field) and one IMAD per plane:
+// about 1.0-1.5 ALU ops per comparison at W = 16, against the POPC pipe's
+// 16/clk/SM bound of a per-pair XOR + POPC.
+//
+// sig' (internal, exact).  Bytes that are NOT scheme letters are hashed into S
+// extra one-bit occurrence fields (host LUT, frequency round robin).  One edit
+// involves at most two symbols and each symbol owns at most one field of
+// (scheme fields + sig' fields), so F_D + F_sig' <= 2 * distance for every
+// variant / metric pair the reference filters with (occurrence, count:
+// Hamming + Levenshtein; halved, position: Hamming).  Counting on through the
+// sig' planes with the same counters therefore never drops a match; it only
+// shrinks the candidate set the byte verifier sees.  QueryStats use the
+// counters as they stand after the scheme planes (the reference's F_D alone).
+//
+// Candidates (rare) go to a lane-private queue in shared memory as
+// (query, slab, 32-bit word mask) and are byte-verified at k <= 1
+// (edit_distance.hpp:18-64) in batches; matches leave through a
+// warp-aggregated atomic append as (query id << 32 | word id) keys for K4.
+#pragma once
+
+#include <cstdint>
+#include <type_traits>
+
+namespace fpg {
+
+constexpr int kSliceThreads = 256;
+constexpr int kSliceWarps = kSliceThreads / 32;
+constexpr int kSliceQ = 128;      // queries per tile (shared-memory masks)
+constexpr int kSliceCap = 8;      // queue entries per lane
+constexpr int kSliceWarpBuf = 256;  // expanded candidates per warp and verify round
+
+__host__ __device__ constexpr int slice_slabs_per_lane(int npt) { return npt <= 32 ? 2 : 1; }
+
+struct SliceTile {
+    uint32_t slab_begin;   // first slab of the tile, bucket-local
+    uint32_t n_slabs;      // slabs in the tile (<= 256 * SL)
+    uint32_t q_begin;      // sorted query positions [q_begin, q_begin + q_count)
+    uint32_t q_count;
+    uint64_t plane_base;   // u32 offset of the bucket's planes
+    uint64_t w_bytes;      // byte offset of the bucket in the padded word blob
+    uint32_t ns;           // slabs in the bucket (plane row length)
+    uint32_t w_start;      // sorted position of the bucket's first word
+    uint32_t w_count;      // words in the bucket
+    uint16_t w_len, w_stride;
+    uint32_t count_only;   // fingerprint survivors counted, never verified
+    uint32_t pad;
+};
+
+struct SliceParams {
+    const uint32_t* planes;     // dictionary planes
+    const uint64_t* q_fp;       // query fingerprints (sorted order)
+    const uint32_t* q_sigp;     // query sig' codes
+    const uint16_t* q_len;      // query lengths (sorted order)
+    const uint32_t* q_start;    // per length: first sorted position
+    const uint64_t* q_bbase;    // per length: byte offset in the padded query blob
+    const uint8_t* q_bytes;
+    const uint32_t* q_ids;
+    const uint8_t* w_bytes;
+    const uint32_t* w_ids;
+    uint64_t id_base;
+    uint32_t* q_survivors;
+    unsigned long long* out;
+    unsigned long long* out_count;
+    unsigned long long* survivors_total;
+    unsigned int* tile_counter;
+    unsigned long long* candidates;  // pairs handed to the byte verifier
+    uint32_t* q_matches;             // per input query: matches (K4 segment sizes)
+    unsigned long long* big_seg;
+    uint64_t out_cap;
+    int32_t k;
+    int32_t stats;
+    int32_t use_fp;             // scheme fields bound this metric (variant_supports, fingerprint.hpp:36-38)
+};
+
+__device__ __forceinline__ int stride_of_len(int len) { return len <= 16 ? 16 : (len + 15) & ~15; }
+
+// x = p XOR (query bit): s = 1, m = 0 keeps p; s = -1, m = ~0 gives ~p.
+__device__ __forceinline__ uint32_t qxor(uint32_t p, uint32_t s, uint32_t m) { return p * s + m; }
+
+template <int NP, int FW, int EXTRA, int S>
+struct SliceShape {
+    static constexpr int NPT = NP + S;
+    static constexpr int SL = slice_slabs_per_lane(NPT);
+    static constexpr int NF = (NP - EXTRA) / FW;
+    static_assert(NF * FW + EXTRA == NP, "field layout");
+    static_assert(NPT % 2 == 0, "plane pairs");
+};
+
+// Dynamic shared memory of k_slice<NP, .., S>.
+__host__ __device__ constexpr size_t slice_smem_bytes(int npt) {
+    return (size_t)kSliceQ * npt * 8 + 32u * kSliceQ + 8u * kSliceQ + 8u * kSliceCap * kSliceThreads +
+           4u * kSliceWarpBuf * kSliceWarps;
+}
+
+template <int NP, int FW, int EXTRA, int S>
+__global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __restrict__ tiles, uint32_t ntiles,
+                                                            const __grid_constant__ SliceParams P) {
+    using Sh = SliceShape<NP, FW, EXTRA, S>;
+    constexpr int NPT = Sh::NPT, SL = Sh::SL, NF = Sh::NF;
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint2* s_qm = reinterpret_cast<uint2*>(smem);                           // [kSliceQ][NPT] (s, m)
+    uint4* s_qb = reinterpret_cast<uint4*>(s_qm + kSliceQ * NPT);           // [kSliceQ][2]: bytes 0..31
+    uint32_t* s_qinfo = reinterpret_cast<uint32_t*>(s_qb + 2 * kSliceQ);    // [kSliceQ]: length
+    uint32_t* s_qid = s_qinfo + kSliceQ;                                    // [kSliceQ]: input query id
+    uint2* s_queue = reinterpret_cast<uint2*>(s_qid + kSliceQ);             // [cap][threads]
+    uint32_t* s_wbuf = reinterpret_cast<uint32_t*>(s_queue + kSliceCap * kSliceThreads);  // [warps][buf]
+    __shared__ uint32_t s_tile;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    unsigned long long surv_warp = 0;
+    uint32_t cand_lane = 0;
+
+    for (;;) {
+        __syncthreads();  // previous tile fully consumed
+        if (tid == 0) s_tile = atomicAdd(P.tile_counter, 1u);
+        __syncthreads();
+        const uint32_t t = s_tile;
+        if (t >= ntiles) break;
+        const SliceTile tl = tiles[t];
+
+        // query (s, m) masks
+        for (uint32_t i = tid; i < tl.q_count * NPT; i += kSliceThreads) {
+            const uint32_t j = i / NPT, b = i - j * NPT;
+            const uint32_t qp = tl.q_begin + j;
+            const uint32_t bit = b < (uint32_t)NP ? (uint32_t)(__ldg(P.q_fp + qp) >> b) & 1u
+                                                  : (__ldg(P.q_sigp + qp) >> (b - NP)) & 1u;
+            s_qm[i] = bit ? make_uint2(0xffffffffu, 0xffffffffu) : make_uint2(1u, 0u);
+        }
+        // query bytes (first 32, zero padded) and lengths for the verifier
+        for (uint32_t i = tid; i < 2 * tl.q_count; i += kSliceThreads) {
+            const uint32_t j = i >> 1, h = i & 1;
+            const uint32_t qp = tl.q_begin + j;
+            const int m = P.q_len[qp];
+            const int qs = stride_of_len(m);
+            const uint8_t* qb = P.q_bytes + P.q_bbase[m] + (uint64_t)(qp - P.q_start[m]) * qs;
+            s_qb[i] = (16 * h < (uint32_t)qs) ? __ldg(reinterpret_cast<const uint4*>(qb) + h) : make_uint4(0, 0, 0, 0);
+            if (h == 0) {
+                s_qinfo[j] = (uint32_t)m;
+                s_qid[j] = P.q_ids[qp];
+            }
+        }
+        // this lane's slabs: tl.slab_begin + tid + 256 r
+        uint32_t pl[SL][NPT];
+        uint32_t valid[SL];
+#pragma unroll
+        for (int r = 0; r < SL; ++r) {
+            const uint32_t rel = (uint32_t)tid + kSliceThreads * r;
+            const uint32_t slab = tl.slab_begin + rel;
+            const bool ok = rel < tl.n_slabs;
+            const uint32_t* src = P.planes + tl.plane_base + slab;
+#pragma unroll
+            for (int b = 0; b < NPT; ++b) pl[r][b] = ok ? __ldg(src + (size_t)b * tl.ns) : 0u;
+            const uint32_t rem = tl.w_count - 32u * slab;  // words left in the bucket from this slab on
+            valid[r] = !ok ? 0u : rem >= 32u ? 0xffffffffu : ((1u << rem) - 1u);
+        }
+        __syncthreads();
+
+        uint32_t qn = 0;  // queued entries of this lane
+        const bool verify = !tl.count_only;
+
+        // Byte-verifies the queued (query, slab, mask) candidates of the warp.
+        // Byte-verifies the warp's queued candidates.  The lanes' (query, slab,
+        // mask) entries are first expanded into a warp-wide list of single
+        // (query, word) candidates (rounds of <= kSliceWarpBuf), which the 32
+        // lanes then verify side by side, one candidate each.
+        uint32_t* wbuf = s_wbuf + warp * kSliceWarpBuf;
+        auto flush = [&]() {
+            __syncwarp();
+            for (;;) {
+                // pending candidate bits of this lane
+                uint32_t c = 0;
+                for (uint32_t s = 0; s < qn; ++s) c += __popc(s_queue[s * kSliceThreads + tid].y);
+                uint32_t incl = c;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (lane >= d) incl += v;
+                }
+                const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+                if (total == 0) break;
+                // this lane's candidates take ranks [incl - c, incl); those < kSliceWarpBuf go now
+                uint32_t rank = incl - c;
+                for (uint32_t s = 0; s < qn && rank < (uint32_t)kSliceWarpBuf; ++s) {
+                    uint2 e = s_queue[s * kSliceThreads + tid];
+                    const uint32_t j = e.x & 0xffffu, r = e.x >> 16;
+                    const uint32_t wt0 = 32u * ((uint32_t)tid + kSliceThreads * r);  // word index within the tile
+                    while (e.y && rank < (uint32_t)kSliceWarpBuf) {
+                        const int i = __ffs(e.y) - 1;
+                        e.y &= e.y - 1;
+                        wbuf[rank++] = (j << 16) | (wt0 + (uint32_t)i);
+                    }
+                    s_queue[s * kSliceThreads + tid].y = e.y;
+                }
+                __syncwarp();
+                const uint32_t m_all = min(total, (uint32_t)kSliceWarpBuf);
+                cand_lane += (lane == 0) ? m_all : 0u;
+                for (uint32_t base = 0; base < m_all; base += 32) {
+                    const uint32_t idx = base + lane;
+                    bool hit = false;
+                    uint32_t j = 0, widx = 0;
+                    if (idx < m_all) {
+                        const uint32_t v = wbuf[idx];
+                        j = v >> 16;
+                        widx = 32u * tl.slab_begin + (v & 0xffffu);
+                        const int m = (int)s_qinfo[j], n = tl.w_len;
+                        const int ws = tl.w_stride;
+                        const uint8_t* wb = P.w_bytes + tl.w_bytes + (uint64_t)widx * ws;
+                        const int mx = m > n ? m : n;
+                        if (mx <= 16) {
+                            uint32_t a[4], bb[4];
+                            const uint4 qa = s_qb[2 * j];
+                            a[0] = qa.x; a[1] = qa.y; a[2] = qa.z; a[3] = qa.w;
+                            load_padded<4>(wb, ws, bb);
+                            hit = verify_regs<4>(a, bb, m, n, P.k);
+                        } else if (mx <= 32) {
+                            uint32_t a[8], bb[8];
+                            const uint4 qa = s_qb[2 * j], qc = s_qb[2 * j + 1];
+                            a[0] = qa.x; a[1] = qa.y; a[2] = qa.z; a[3] = qa.w;
+                            a[4] = qc.x; a[5] = qc.y; a[6] = qc.z; a[7] = qc.w;
+                            load_padded<8>(wb, ws, bb);
+                            hit = verify_regs<8>(a, bb, m, n, P.k);
+                        } else {
+                            const uint32_t qpos = tl.q_begin + j;
+                            const int qs = stride_of_len(m);
+                            const uint8_t* qb = P.q_bytes + P.q_bbase[m] + (uint64_t)(qpos - P.q_start[m]) * qs;
+                            hit = verify_pair(qb, m, qs, wb, n, ws, P.k);
+                        }
+                    }
+                    const uint32_t hb = __ballot_sync(0xffffffffu, hit);
+                    if (hb) {
+                        unsigned long long slot = 0;
+                        if (lane == 0) slot = atomicAdd(P.out_count, (unsigned long long)__popc(hb));
+                        slot = __shfl_sync(0xffffffffu, slot, 0);
+                        if (hit) {
+                            const uint64_t o = slot + __popc(hb & lt_mask);
+                            if (o < P.out_cap) {
+                                const uint64_t qid = s_qid[j];
+                                const uint64_t wid = P.id_base + P.w_ids[tl.w_start + widx];
+                                P.out[o] = (qid << 32) | wid;
+                            }
+                            count_match(P.q_matches, P.big_seg, s_qid[j]);
+                        }
+                    }
+                }
+                __syncwarp();
+                if (total <= (uint32_t)kSliceWarpBuf) break;
+            }
+            qn = 0;
+        };
+
+        // Per-warp slab count: warps whose second slab row is empty (a
+        // bucket's last chunk) run the one-slab loop instead of scanning zeros.
+        auto scan_queries = [&](auto slc) {
+            constexpr int SLX = decltype(slc)::value;
+            for (uint32_t j = 0; j < tl.q_count; ++j) {
+                const uint4* qm = reinterpret_cast<const uint4*>(s_qm + j * NPT);
+                uint32_t c0[SLX], c1[SLX], c2[SLX];
+#pragma unroll
+                for (int r = 0; r < SLX; ++r) c0[r] = c1[r] = c2[r] = 0u;
+                // (s, m) of plane b
+#define FPG_QS(b) ((b) & 1 ? qm[(b) >> 1].z : qm[(b) >> 1].x)
+#define FPG_QM(b) ((b) & 1 ? qm[(b) >> 1].w : qm[(b) >> 1].y)
+                // scheme fields: NF fields of FW planes above EXTRA one-bit fields.
+                // Skipped when they do not bound the metric (halved / position with
+                // Levenshtein, filter off): sig' alone stays a valid bound.
+                if (P.use_fp) {
+#pragma unroll
+                for (int f = 0; f < NF; ++f) {
+                    const int b0 = EXTRA + FW * f;
+#pragma unroll
+                    for (int r = 0; r < SLX; ++r) {
+                        uint32_t x = qxor(pl[r][b0], FPG_QS(b0), FPG_QM(b0));
+#pragma unroll
+                        for (int u = 1; u < FW; ++u) x |= qxor(pl[r][b0 + u], FPG_QS(b0 + u), FPG_QM(b0 + u));
+                        c2[r] |= c1[r] & x;
+                        c1[r] |= c0[r] & x;
+                        c0[r] |= x;
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e < EXTRA; ++e) {
+#pragma unroll
+                    for (int r = 0; r < SLX; ++r) {
+                        const uint32_t x = qxor(pl[r][e], FPG_QS(e), FPG_QM(e));
+                        c2[r] |= c1[r] & x;
+                        c1[r] |= c0[r] & x;
+                        c0[r] |= x;
+                    }
+                }
+                }
+                if (P.stats) {  // fingerprint survivors: QueryStats::verified (dictionary.hpp:102-110)
+                    uint32_t sv = 0;
+#pragma unroll
+                    for (int r = 0; r < SLX; ++r) sv += __popc(valid[r] & ~(P.k ? c2[r] : c0[r]));
+                    sv = __reduce_add_sync(0xffffffffu, sv);
+                    if (lane == 0 && sv) atomicAdd(&P.q_survivors[s_qid[j]], sv);
+                    surv_warp += sv;
+                }
+                if (verify) {
+#pragma unroll
+                    for (int g = 0; g < S; ++g) {
+#pragma unroll
+                        for (int r = 0; r < SLX; ++r) {
+                            const uint32_t x = qxor(pl[r][NP + g], FPG_QS(NP + g), FPG_QM(NP + g));
+                            c2[r] |= c1[r] & x;
+                            c1[r] |= c0[r] & x;
+                            c0[r] |= x;
+                        }
+                    }
+#undef FPG_QS
+#undef FPG_QM
+#pragma unroll
+                    for (int r = 0; r < SLX; ++r) {
+                        const uint32_t cand = valid[r] & ~(P.k ? c2[r] : c0[r]);
+                        if (cand) {
+                            s_queue[qn * kSliceThreads + tid] = make_uint2(j | ((uint32_t)r << 16), cand);
+                            ++qn;
+                        }
+                    }
+                    if (__any_sync(0xffffffffu, qn > (uint32_t)(kSliceCap - SLX))) flush();
+                }
+            }
+        };
+        if (SL == 2 && 32u * warp + kSliceThreads < tl.n_slabs) scan_queries(std::integral_constant<int, SL>{});
+        else scan_queries(std::integral_constant<int, 1>{});
+        if (verify) flush();
+    }
+    if (P.stats && lane == 0 && surv_warp) atomicAdd(P.survivors_total, surv_warp);
+    cand_lane = __reduce_add_sync(0xffffffffu, cand_lane);
+    if (lane == 0 && cand_lane) atomicAdd(P.candidates, (unsigned long long)cand_lane);
+}
+
+// ---------------------------------------------------------------- K1b planes
+// One warp per slab: lane i holds word 32 s + i of its bucket; plane b is the
+// ballot of bit b of the words' codes (fingerprint bits, then sig' bits).
+__global__ void k_planes(const uint64_t* __restrict__ fp, const uint32_t* __restrict__ sigp,
+                         const uint32_t* __restrict__ slab_start,  // per length: first global slab (L1 + 1)
+                         const uint32_t* __restrict__ start,       // per length: first sorted position
+                         const uint32_t* __restrict__ count,       // per length: words
+                         const uint64_t* __restrict__ plane_base,  // per length: u32 offset of the planes
+                         int nlen, uint32_t total_slabs, int np, int npt, uint32_t* __restrict__ planes) {
+    const uint32_t gs = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (gs >= total_slabs) return;
+    int lo = 0, hi = nlen;  // largest L with slab_start[L] <= gs
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (slab_start[mid] <= gs) lo = mid;
+        else hi = mid;
+    }
+    const int L = lo;
+    const uint32_t s = gs - slab_start[L];
+    const uint32_t ns = slab_start[L + 1] - slab_start[L];
+    const uint32_t w = 32u * s + lane;
+    const bool ok = w < count[L];
+    const uint64_t f = ok ? fp[start[L] + w] : 0ull;
+    const uint32_t g = ok ? sigp[start[L] + w] : 0u;
+    uint32_t mine[3] = {0u, 0u, 0u};
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+            const int b = 32 * r + t;
+            if (b < npt) {  // warp-uniform
+                const uint32_t bit = b < np ? (uint32_t)(f >> b) & 1u : (g >> (b - np)) & 1u;
+                const uint32_t ball = __ballot_sync(0xffffffffu, bit != 0);
+                if (lane == t) mine[r] = ball;
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        const int b = 32 * r + lane;
+        if (b < npt) planes[plane_base[L] + (uint64_t)b * ns + s] = mine[r];
+    }
+}
+
+// 256-bin byte histogram of a blob (sig' symbol ranking).
+__global__ void k_hist256(const uint8_t* __restrict__ blob, uint64_t n, unsigned long long* __restrict__ hist) {
+    __shared__ unsigned int h[256];
+    h[threadIdx.x] = 0;  // blockDim == 256
+    __syncthreads();
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        atomicAdd(&h[blob[i]], 1u);
+    __syncthreads();
+    if (h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], (unsigned long long)h[threadIdx.x]);
+}
+
+}  // namespace fpg

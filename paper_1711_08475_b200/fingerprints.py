@@ -485,8 +485,10 @@ class Batch:
         ex, sv, ln = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
         check(self._lib.fpg_batch_last_timing(self._h, shard, ctypes.byref(run_ms), ctypes.byref(filt_ms),
                                               ctypes.byref(ex), ctypes.byref(sv), ctypes.byref(ln)))
+        cand = ctypes.c_uint64()
+        check(self._lib.fpg_batch_last_candidates(self._h, shard, ctypes.byref(cand)))
         return {"run_ms": run_ms.value, "filter_ms": filt_ms.value, "executed_pairs": ex.value,
-                "survivors": sv.value, "launches": ln.value}
+                "survivors": sv.value, "launches": ln.value, "candidates": cand.value}
 
     def close(self) -> None:
         if getattr(self, "_h", None):
