@@ -41,6 +41,35 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 POPC_PER_CLK_PER_SM = 16  # measured: tools/microbench/intpipe.cu (profiles/r01_phase0.txt)
+ALU_PER_CLK_PER_SM = 64   # LOP3 issue: 16 lanes/clk/SMSP (B300_MICROARCH.md "Pipe rates")
+
+
+def ops_per_comparison(scheme, sig_fields: int) -> float:
+    """LOP3 per comparison of the bit-sliced test (fpg_slice.cuh): per 32-word
+    slab, 3 counter updates per field plus the ORs folding a multi-bit
+    field's planes (1 for 2-3 bits, 2 for 4 bits); sig' planes are one-bit fields."""
+    v, w = scheme.variant().name, scheme.width()
+    if v == "Count":
+        fw, extra = scheme.bits_per_count(), 0
+    elif v == "Position":
+        fw = scheme.bits_per_position()
+        extra = w % fw
+    else:
+        fw, extra = 1, 0
+    nf = (w - extra) // fw
+    per_field = 3 + (0 if fw == 1 else 1 if fw <= 3 else 2)
+    return (nf * per_field + 3 * extra + 3 * sig_fields) / 32.0
+
+
+def profiled_traffic(workload: str, cell: str):
+    """DRAM bytes of one K2 launch from the committed ncu --set full capture
+    (profiles/traffic.json, written by tools/ncu_summary.py traffic)."""
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        rec = json.loads(p.read_text()).get(f"{workload} {cell}")
+    except (OSError, ValueError):
+        return None
+    return rec["dram_bytes"] if rec else None
 
 
 def parse():
@@ -308,12 +337,24 @@ def main():
 
     if rank != 0:
         return
-    # roofline of the dominant kernel (K2 filter+verify): executed pairs per launch / launch time
+    # roofline of the dominant kernel (K2): executed (length-compatible) pairs
+    # per launch / the launch's CUDA-event time, against the ALU-pipe bound of
+    # the bit-sliced test
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     sm_mhz = clk.get("sm_max_mhz") or 1965.0
-    peak = sms * sm_mhz * 1e6 * POPC_PER_CLK_PER_SM / math.ceil(scheme.width() / 32) / 1e12
     filt_avg_ms = statistics.mean(filt_ms)
     achieved = executed / (filt_avg_ms / 1e3) / 1e12
+    shape = d.scan_shape()
+    ops = ops_per_comparison(scheme, shape["sig_fields"])
+    popc_peak = sms * sm_mhz * 1e6 * POPC_PER_CLK_PER_SM / math.ceil(scheme.width() / 32) / 1e12
+    if shape["sliced"]:
+        peak = sms * sm_mhz * 1e6 * ALU_PER_CLK_PER_SM / ops / 1e12
+        bound, basis = "int-alu", (f"{sms} SMs x {sm_mhz:.0f} MHz x {ALU_PER_CLK_PER_SM} LOP3/clk/SM / "
+                                   f"{ops:.3f} LOP3 per comparison (bit-sliced test, {shape['sig_fields']} sig' planes)")
+    else:
+        peak = popc_peak
+        bound, basis = "int-xu", f"{sms} SMs x {sm_mhz:.0f} MHz x {POPC_PER_CLK_PER_SM} POPC/clk/SM / ceil(W/32)"
+    traffic = profiled_traffic(f"config{args.config}", _cell_name(args.config, args.cell))
     line = {
         "metric": "k=1 query x word comparisons/s (logical Q*N)",
         "value": value, "unit": "comparisons/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -330,11 +371,12 @@ def main():
         "construction_s": build_s,
         "gpu_launches": launches,
         "e2e": {"value": e2e_value, "unit": "comparisons/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "roofline": {"bound": "int", "kernel": "k_scan (K2 filter+verify)", "achieved": achieved,
-                     "peak": peak, "unit": "Tcmp/s", "frac": achieved / peak, "traffic": None,
-                     "peak_basis": f"{sms} SMs x {sm_mhz:.0f} MHz x {POPC_PER_CLK_PER_SM} POPC/clk/SM / ceil(W/32) "
-                                   "(POPC rate measured by tools/microbench/intpipe.cu)",
-                     "filter_ms_per_launch": filt_avg_ms},
+        "roofline": {"bound": bound, "kernel": "k_slice (K2 filter+verify)" if shape["sliced"] else "k_scan (K2)",
+                     "achieved": achieved, "peak": peak, "unit": "Tcmp/s", "frac": achieved / peak,
+                     "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",
+                     "peak_basis": basis,
+                     "popc_equiv_peak": popc_peak, "popc_equiv_frac": achieved / popc_peak,
+                     "filter_ms_per_launch": filt_avg_ms, "filter_share_of_step": filt_avg_ms / ms_per_step},
         "clocks": clk,
     }
     if not args.no_cpu_baseline:

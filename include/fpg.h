@@ -144,6 +144,10 @@ int fpg_batch_last_timing(const fpg_batch* batch, int32_t shard, double* run_ms,
                           double* filter_ms, uint64_t* executed_pairs, uint64_t* survivors,
                           uint64_t* kernel_launches);
 
+/* Shape of the dictionary's K2 path: *sliced = 1 for the bit-sliced k_slice
+ * (0: generic per-pair k_scan), *sig_fields = S extra sig' planes. */
+int fpg_dict_scan_shape(const fpg_dict* dict, int32_t* sliced, int32_t* sig_fields);
+
 /* Pairs of the last run on `shard` that reached the byte verifier (after
  * the fingerprint test and the verifier's own exact pre-filters). */
 int fpg_batch_last_candidates(const fpg_batch* batch, int32_t shard, uint64_t* candidates);

@@ -85,6 +85,8 @@ FPG_SIGNATURES = {
                                              ctypes.POINTER(ctypes.c_double), c_u64p, c_u64p,
                                              c_u64p]),
     "fpg_batch_last_candidates": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, c_u64p]),
+    "fpg_dict_scan_shape": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32),
+                                           ctypes.POINTER(ctypes.c_int32)]),
 }
 
 FPG_OK, FPG_EINVAL, FPG_EUNSUPPORTED, FPG_ECUDA, FPG_ENOMEM = 0, -1, -2, -3, -4

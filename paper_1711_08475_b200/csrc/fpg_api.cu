@@ -396,6 +396,10 @@ struct ShardBatch {
     Collection queries;
     DBuf<fpg::Tile> tiles;
     DBuf<fpg::SliceTile> stiles;
+    std::vector<fpg::Tile> plan;
+    std::vector<fpg::SliceTile> splan;
+    bool plan_valid = false;
+    fpg_query_options plan_opts{};
     DBuf<unsigned long long> out, sorted;
     DBuf<unsigned long long> counters;  // [0] out_count, [1] survivors_total, [2] tile counter
     DBuf<uint32_t> qsurv;
@@ -523,12 +527,16 @@ void launch_slice(const fpg::SliceTile* tiles, uint32_t ntiles, const fpg::Slice
                   int device) {
     auto kern = fpg::k_slice<NP, FW, EXTRA, S>;
     constexpr size_t smem = fpg::slice_smem_bytes(NP + S);
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, fpg::kSliceThreads, smem));
-    const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)sms * std::max(per_sm, 1));
+    static int resident[64] = {0};  // per device: CTAs resident on the whole GPU (0 = not yet queried)
+    const int dv = device & 63;
+    if (!resident[dv]) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int sms = 148, per_sm = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, fpg::kSliceThreads, smem));
+        resident[dv] = sms * std::max(per_sm, 1);
+    }
+    const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)resident[dv]);
     kern<<<(unsigned)std::max<uint64_t>(grid, 1), fpg::kSliceThreads, smem, st>>>(tiles, ntiles, P);
     CK(cudaGetLastError());
 }
@@ -601,10 +609,15 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
     const Collection& W = sh.dict;
     const bool count_only_pass = o.want_stats && o.use_filter && o.metric == FPG_LEVENSHTEIN && !o.length_prefilter;
     uint64_t executed = 0;
-    std::vector<fpg::Tile> plan;
-    std::vector<fpg::SliceTile> splan;
-
-    if (D->slice) {
+    std::vector<fpg::Tile>& plan = S.plan;
+    std::vector<fpg::SliceTile>& splan = S.splan;
+    // The tile plan depends only on the uploaded batch and the options: it is
+    // built (and uploaded) on the first run of a batch and reused after.
+    const bool replan = !S.plan_valid || std::memcmp(&S.plan_opts, &o, sizeof(o)) != 0;
+    if (!replan) {
+        executed = S.executed;
+    } else if (D->slice) {
+        splan.clear();
         // Tile plan: per word length lw, the compatible query lengths form one
         // contiguous range of the length-sorted queries (Hamming / k = 0:
         // lw; Levenshtein k = 1: lw - 1 .. lw + 1, edit_distance.hpp:38-39).
@@ -612,19 +625,7 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         // handed out by an atomic counter.
         const uint32_t chunk = fpg::kSliceThreads * fpg::slice_slabs_per_lane(D->npt);
         const int L1 = fpg::kMaxLen + 1;
-        // query chunk: the largest of 128 / 64 / 32 that still gives every
-        // resident CTA (2 per SM) about 8 tiles, so the dynamic schedule ends evenly
-        uint64_t units = 0;  // (query, slab-chunk) units of the verified ranges
-        for (int lw = 0; lw <= W.max_len; ++lw) {
-            if (!W.count[lw]) continue;
-            const int span = (o.metric == FPG_HAMMING) ? 0 : o.k;
-            const int lo = std::max(0, lw - span), hi = std::min(L1 - 1, lw + span);
-            units += (uint64_t)(Q.start[hi] + Q.count[hi] - Q.start[lo]) * cdiv(cdiv(W.count[lw], 32), chunk);
-        }
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, sh.device);
-        uint32_t qchunk = fpg::kSliceQ;
-        while (qchunk > 32 && units / qchunk < (uint64_t)sms * 2 * 8) qchunk >>= 1;
+        const uint32_t qchunk = fpg::kSliceQ;
         auto add = [&](int lw, uint32_t qb, uint32_t qe, bool count_only) {
             const uint32_t ns = (uint32_t)cdiv(W.count[lw], 32);
             for (uint32_t q0 = qb; q0 < qe; q0 += qchunk)
@@ -657,15 +658,36 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
                 add(lw, qe, (uint32_t)nq, true);
             }
         }
-        std::stable_sort(splan.begin(), splan.end(), [](const fpg::SliceTile& x, const fpg::SliceTile& y) {
-            return (uint64_t)x.q_count * x.n_slabs > (uint64_t)y.q_count * y.n_slabs;
-        });
+        // Largest tiles first; the last ~30% of the work is cut into quarter
+        // tiles so the dynamically scheduled grid drains evenly.
+        auto cost = [](const fpg::SliceTile& x) { return (uint64_t)x.q_count * x.n_slabs; };
+        std::stable_sort(splan.begin(), splan.end(),
+                         [&](const fpg::SliceTile& x, const fpg::SliceTile& y) { return cost(x) > cost(y); });
+        uint64_t work = 0, acc = 0;
+        for (const auto& t : splan) work += cost(t);
+        std::vector<fpg::SliceTile> fine;
+        fine.reserve(splan.size() + splan.size() / 2);
+        for (const auto& t : splan) {
+            acc += cost(t);
+            if (acc * 10 <= work * 7 || t.q_count <= 32) {
+                fine.push_back(t);
+                continue;
+            }
+            for (uint32_t q0 = 0; q0 < t.q_count; q0 += 32) {
+                fpg::SliceTile u = t;
+                u.q_begin = t.q_begin + q0;
+                u.q_count = std::min<uint32_t>(32, t.q_count - q0);
+                fine.push_back(u);
+            }
+        }
+        splan.swap(fine);
         S.stiles.reserve(splan.size());
         if (!splan.empty())
             CK(cudaMemcpyAsync(S.stiles.p, splan.data(), splan.size() * sizeof(fpg::SliceTile),
                                cudaMemcpyHostToDevice, st));
     } else {
         // Generic k_scan: one tile per (query length, word length) bucket pair block.
+        plan.clear();
         for (int lq = 0; lq <= Q.max_len; ++lq) {
             if (!Q.count[lq]) continue;
             for (int lw = 0; lw <= W.max_len; ++lw) {
@@ -697,6 +719,8 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
             CK(cudaMemcpyAsync(S.tiles.p, plan.data(), plan.size() * sizeof(fpg::Tile), cudaMemcpyHostToDevice, st));
     }
     S.executed = executed;
+    S.plan_valid = true;
+    S.plan_opts = o;
 
     fpg::ScanParams P{};
     fpg::SliceParams SP{};
@@ -887,6 +911,7 @@ void upload(fpg_batch* B, const uint8_t* qbytes, const uint64_t* qoffsets, uint6
         S.qblob.reserve(nbytes + 16);
         S.qoffs.reserve(nq + 1);
         S.qorder.reserve(nq);
+        S.plan_valid = false;
         Collection& Q = S.queries;
         Q.n = nq;
         Q.count = B->qcount;
@@ -1240,6 +1265,14 @@ int fpg_batch_last_timing(const fpg_batch* batch, int32_t shard, double* run_ms,
         if (executed_pairs) *executed_pairs = S.executed;
         if (survivors) *survivors = S.survivors;
         if (kernel_launches) *kernel_launches = S.launches;
+    });
+}
+
+int fpg_dict_scan_shape(const fpg_dict* dict, int32_t* sliced, int32_t* sig_fields) {
+    return guarded([&] {
+        if (!dict || !sliced || !sig_fields) throw Error(FPG_EINVAL, "null argument");
+        *sliced = dict->slice ? 1 : 0;
+        *sig_fields = dict->params.nsig;
     });
 }
 

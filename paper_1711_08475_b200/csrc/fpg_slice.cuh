@@ -126,40 +126,42 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
     uint32_t* s_qid = s_qinfo + kSliceQ;                                    // [kSliceQ]: input query id
     uint2* s_queue = reinterpret_cast<uint2*>(s_qid + kSliceQ);             // [cap][threads]
     uint32_t* s_wbuf = reinterpret_cast<uint32_t*>(s_queue + kSliceCap * kSliceThreads);  // [warps][buf]
-    __shared__ uint32_t s_tile;
+    __shared__ uint32_t s_next[2];  // next tile index, double-buffered by iteration parity
+    __shared__ uint32_t s_surv[kSliceQ];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
     unsigned long long surv_warp = 0;
     uint32_t cand_lane = 0;
 
-    for (;;) {
-        __syncthreads();  // previous tile fully consumed
-        if (tid == 0) s_tile = atomicAdd(P.tile_counter, 1u);
-        __syncthreads();
-        const uint32_t t = s_tile;
-        if (t >= ntiles) break;
+    if (tid == 0) s_next[0] = atomicAdd(P.tile_counter, 1u);
+    __syncthreads();
+    uint32_t t = s_next[0];
+    for (uint32_t it = 1; t < ntiles; ++it) {
         const SliceTile tl = tiles[t];
+        if (tid == 0) s_next[it & 1] = atomicAdd(P.tile_counter, 1u);  // read after the end-of-tile barrier
 
-        // query (s, m) masks
-        for (uint32_t i = tid; i < tl.q_count * NPT; i += kSliceThreads) {
-            const uint32_t j = i / NPT, b = i - j * NPT;
+        // query (s, m) masks, verifier bytes / lengths / ids; one query per thread
+        for (uint32_t j = tid; j < tl.q_count; j += kSliceThreads) {
             const uint32_t qp = tl.q_begin + j;
-            const uint32_t bit = b < (uint32_t)NP ? (uint32_t)(__ldg(P.q_fp + qp) >> b) & 1u
-                                                  : (__ldg(P.q_sigp + qp) >> (b - NP)) & 1u;
-            s_qm[i] = bit ? make_uint2(0xffffffffu, 0xffffffffu) : make_uint2(1u, 0u);
-        }
-        // query bytes (first 32, zero padded) and lengths for the verifier
-        for (uint32_t i = tid; i < 2 * tl.q_count; i += kSliceThreads) {
-            const uint32_t j = i >> 1, h = i & 1;
-            const uint32_t qp = tl.q_begin + j;
+            const uint64_t f = __ldg(P.q_fp + qp);
+            const uint32_t g = __ldg(P.q_sigp + qp);
             const int m = P.q_len[qp];
             const int qs = stride_of_len(m);
-            const uint8_t* qb = P.q_bytes + P.q_bbase[m] + (uint64_t)(qp - P.q_start[m]) * qs;
-            s_qb[i] = (16 * h < (uint32_t)qs) ? __ldg(reinterpret_cast<const uint4*>(qb) + h) : make_uint4(0, 0, 0, 0);
-            if (h == 0) {
-                s_qinfo[j] = (uint32_t)m;
-                s_qid[j] = P.q_ids[qp];
+            const uint4* qb = reinterpret_cast<const uint4*>(P.q_bytes + P.q_bbase[m] + (uint64_t)(qp - P.q_start[m]) * qs);
+            const uint4 b0 = __ldg(qb);
+            const uint4 b1 = qs > 16 ? __ldg(qb + 1) : make_uint4(0, 0, 0, 0);
+            const uint32_t id = P.q_ids[qp];
+            uint2* dst = s_qm + j * NPT;
+#pragma unroll
+            for (int b = 0; b < NPT; ++b) {
+                const uint32_t bit = b < NP ? (uint32_t)(f >> b) & 1u : (g >> (b - NP)) & 1u;
+                dst[b] = bit ? make_uint2(0xffffffffu, 0xffffffffu) : make_uint2(1u, 0u);
             }
+            s_qb[2 * j] = b0;
+            s_qb[2 * j + 1] = b1;
+            s_qinfo[j] = (uint32_t)m;
+            s_qid[j] = id;
+            s_surv[j] = 0u;
         }
         // this lane's slabs: tl.slab_begin + tid + 256 r
         uint32_t pl[SL][NPT];
@@ -180,7 +182,6 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
         uint32_t qn = 0;  // queued entries of this lane
         const bool verify = !tl.count_only;
 
-        // Byte-verifies the queued (query, slab, mask) candidates of the warp.
         // Byte-verifies the warp's queued candidates.  The lanes' (query, slab,
         // mask) entries are first expanded into a warp-wide list of single
         // (query, word) candidates (rounds of <= kSliceWarpBuf), which the 32
@@ -315,7 +316,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
 #pragma unroll
                     for (int r = 0; r < SLX; ++r) sv += __popc(valid[r] & ~(P.k ? c2[r] : c0[r]));
                     sv = __reduce_add_sync(0xffffffffu, sv);
-                    if (lane == 0 && sv) atomicAdd(&P.q_survivors[s_qid[j]], sv);
+                    if (lane == 0 && sv) atomicAdd(&s_surv[j], sv);
                     surv_warp += sv;
                 }
                 if (verify) {
@@ -346,6 +347,11 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
         if (SL == 2 && 32u * warp + kSliceThreads < tl.n_slabs) scan_queries(std::integral_constant<int, SL>{});
         else scan_queries(std::integral_constant<int, 1>{});
         if (verify) flush();
+        __syncthreads();  // tile consumed; s_next[it & 1] and s_surv complete
+        if (P.stats)
+            for (uint32_t j = tid; j < tl.q_count; j += kSliceThreads)
+                if (s_surv[j]) atomicAdd(&P.q_survivors[s_qid[j]], s_surv[j]);
+        t = s_next[it & 1];
     }
     if (P.stats && lane == 0 && surv_warp) atomicAdd(P.survivors_total, surv_warp);
     cand_lane = __reduce_add_sync(0xffffffffu, cand_lane);

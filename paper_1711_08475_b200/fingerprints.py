@@ -421,6 +421,12 @@ class GpuFingerprintedDictionary:
     def prints(self) -> list[Fingerprint]:
         return [Fingerprint(int(x)) for x in self.prints_array()]
 
+    def scan_shape(self) -> dict:
+        """K2 path of this dictionary: bit-sliced or generic, and the sig' field count."""
+        sl, sg = ctypes.c_int32(), ctypes.c_int32()
+        check(self._lib.fpg_dict_scan_shape(self._h, ctypes.byref(sl), ctypes.byref(sg)))
+        return {"sliced": bool(sl.value), "sig_fields": sg.value}
+
     def build_seconds(self) -> float:
         s = ctypes.c_double()
         check(self._lib.fpg_dict_build_seconds(self._h, ctypes.byref(s)))

@@ -4,6 +4,7 @@ gpu__time_duration.sum --csv) and/or a --set full report of one kernel.
 
 usage: tools/ncu_summary.py launches <launches.csv>
        tools/ncu_summary.py report <prof.ncu-rep> [<src-lines>]
+       tools/ncu_summary.py traffic <prof.ncu-rep> "<workload> <cell>" profiles/traffic.json
 """
 import collections
 import csv
@@ -80,8 +81,28 @@ def report(path, nlines=25):
         print(f"    {100 * o[0] / ti:5.1f}% {100 * o[1] / ts:5.1f}%  {o[2]}:{o[3]}  {o[4]}")
 
 
+def traffic(path, key, out_json):
+    """Record dram__bytes_read.sum + dram__bytes_write.sum of the captured
+    launch under `key` ("<workload> <cell>") in out_json (bench.py reads it)."""
+    import json
+    import os
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    d, u = dict(zip(hdr, vals)), dict(zip(hdr, units))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot = sum(float(d[k].replace(",", "")) * scale.get(u[k], 1) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    db = json.load(open(out_json)) if os.path.exists(out_json) else {}
+    db[key] = {"kernel": d.get("Kernel Name", "?"), "dram_bytes": tot, "report": os.path.basename(path),
+               "duration_us": float(d["gpu__time_duration.sum"].replace(",", "")) * (1e-3 if u["gpu__time_duration.sum"] == "nsecond" else 1.0)}
+    json.dump(db, open(out_json, "w"), indent=1, sort_keys=True)
+    print(key, db[key])
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2])
+    elif sys.argv[1] == "traffic":
+        traffic(sys.argv[2], sys.argv[3], sys.argv[4])
     else:
         report(sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 25)
