@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
     __shared__ uint32_t s_surv[kSliceQ];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
-    unsigned long long surv_warp = 0;
+    unsigned long long surv_warp = 0;  // lane 0: the warp's fingerprint survivors
     uint32_t cand_lane = 0;
 
     if (tid == 0) s_next[0] = atomicAdd(P.tile_counter, 1u);
@@ -273,76 +273,96 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
 
         // Per-warp slab count: warps whose second slab row is empty (a
         // bucket's last chunk) run the one-slab loop instead of scanning zeros.
-        auto scan_queries = [&](auto slc) {
+        // One step = NQ consecutive queries (j .. j + NQ - 1) against the
+        // lane's SLX slabs: NQ * SLX independent counter chains per plane.
+        auto step = [&](auto slc, auto nqc, uint32_t j) {
             constexpr int SLX = decltype(slc)::value;
-            for (uint32_t j = 0; j < tl.q_count; ++j) {
-                const uint4* qm = reinterpret_cast<const uint4*>(s_qm + j * NPT);
-                uint32_t c0[SLX], c1[SLX], c2[SLX];
+            constexpr int NQ = decltype(nqc)::value;
+            const uint4* qm[NQ];
 #pragma unroll
-                for (int r = 0; r < SLX; ++r) c0[r] = c1[r] = c2[r] = 0u;
-                // (s, m) of plane b
-#define FPG_QS(b) ((b) & 1 ? qm[(b) >> 1].z : qm[(b) >> 1].x)
-#define FPG_QM(b) ((b) & 1 ? qm[(b) >> 1].w : qm[(b) >> 1].y)
-                // scheme fields: NF fields of FW planes above EXTRA one-bit fields.
-                // Skipped when they do not bound the metric (halved / position with
-                // Levenshtein, filter off): sig' alone stays a valid bound.
-                if (P.use_fp) {
+            for (int h = 0; h < NQ; ++h) qm[h] = reinterpret_cast<const uint4*>(s_qm + (j + h) * NPT);
+            uint32_t c0[NQ][SLX], c1[NQ][SLX], c2[NQ][SLX];
+#pragma unroll
+            for (int h = 0; h < NQ; ++h)
+#pragma unroll
+                for (int r = 0; r < SLX; ++r) c0[h][r] = c1[h][r] = c2[h][r] = 0u;
+            // (s, m) of plane b for query h
+#define FPG_QS(h, b) ((b) & 1 ? qm[h][(b) >> 1].z : qm[h][(b) >> 1].x)
+#define FPG_QM(h, b) ((b) & 1 ? qm[h][(b) >> 1].w : qm[h][(b) >> 1].y)
+#define FPG_CNT(h, r, x)            \
+    do {                              \
+        c2[h][r] |= c1[h][r] & (x);   \
+        c1[h][r] |= c0[h][r] & (x);   \
+        c0[h][r] |= (x);              \
+    } while (0)
+            // scheme fields: NF fields of FW planes above EXTRA one-bit fields.
+            // Skipped when they do not bound the metric (halved / position with
+            // Levenshtein, filter off): sig' alone stays a valid bound.
+            if (P.use_fp) {
 #pragma unroll
                 for (int f = 0; f < NF; ++f) {
                     const int b0 = EXTRA + FW * f;
 #pragma unroll
-                    for (int r = 0; r < SLX; ++r) {
-                        uint32_t x = qxor(pl[r][b0], FPG_QS(b0), FPG_QM(b0));
-#pragma unroll
-                        for (int u = 1; u < FW; ++u) x |= qxor(pl[r][b0 + u], FPG_QS(b0 + u), FPG_QM(b0 + u));
-                        c2[r] |= c1[r] & x;
-                        c1[r] |= c0[r] & x;
-                        c0[r] |= x;
-                    }
-                }
-#pragma unroll
-                for (int e = 0; e < EXTRA; ++e) {
-#pragma unroll
-                    for (int r = 0; r < SLX; ++r) {
-                        const uint32_t x = qxor(pl[r][e], FPG_QS(e), FPG_QM(e));
-                        c2[r] |= c1[r] & x;
-                        c1[r] |= c0[r] & x;
-                        c0[r] |= x;
-                    }
-                }
-                }
-                if (P.stats) {  // fingerprint survivors: QueryStats::verified (dictionary.hpp:102-110)
-                    uint32_t sv = 0;
-#pragma unroll
-                    for (int r = 0; r < SLX; ++r) sv += __popc(valid[r] & ~(P.k ? c2[r] : c0[r]));
-                    sv = __reduce_add_sync(0xffffffffu, sv);
-                    if (lane == 0 && sv) atomicAdd(&s_surv[j], sv);
-                    surv_warp += sv;
-                }
-                if (verify) {
-#pragma unroll
-                    for (int g = 0; g < S; ++g) {
+                    for (int h = 0; h < NQ; ++h)
 #pragma unroll
                         for (int r = 0; r < SLX; ++r) {
-                            const uint32_t x = qxor(pl[r][NP + g], FPG_QS(NP + g), FPG_QM(NP + g));
-                            c2[r] |= c1[r] & x;
-                            c1[r] |= c0[r] & x;
-                            c0[r] |= x;
+                            uint32_t x = qxor(pl[r][b0], FPG_QS(h, b0), FPG_QM(h, b0));
+#pragma unroll
+                            for (int u = 1; u < FW; ++u) x |= qxor(pl[r][b0 + u], FPG_QS(h, b0 + u), FPG_QM(h, b0 + u));
+                            FPG_CNT(h, r, x);
                         }
+                }
+#pragma unroll
+                for (int e = 0; e < EXTRA; ++e)
+#pragma unroll
+                    for (int h = 0; h < NQ; ++h)
+#pragma unroll
+                        for (int r = 0; r < SLX; ++r) FPG_CNT(h, r, qxor(pl[r][e], FPG_QS(h, e), FPG_QM(h, e)));
+            }
+            if (P.stats) {  // fingerprint survivors: QueryStats::verified (dictionary.hpp:102-110)
+                uint32_t sv = 0;  // query h in bits [16 h, 16 h + 16): <= 2048 per warp
+#pragma unroll
+                for (int h = 0; h < NQ; ++h)
+#pragma unroll
+                    for (int r = 0; r < SLX; ++r) sv += (uint32_t)__popc(valid[r] & ~(P.k ? c2[h][r] : c0[h][r])) << (16 * h);
+                sv = __reduce_add_sync(0xffffffffu, sv);
+                if (lane == 0) {
+#pragma unroll
+                    for (int h = 0; h < NQ; ++h) {
+                        const uint32_t v = (sv >> (16 * h)) & 0xffffu;
+                        if (v) atomicAdd(&s_surv[j + h], v);
+                        surv_warp += v;
                     }
-#undef FPG_QS
-#undef FPG_QM
+                }
+            }
+            if (verify) {
+#pragma unroll
+                for (int g = 0; g < S; ++g)
+#pragma unroll
+                    for (int h = 0; h < NQ; ++h)
+#pragma unroll
+                        for (int r = 0; r < SLX; ++r) FPG_CNT(h, r, qxor(pl[r][NP + g], FPG_QS(h, NP + g), FPG_QM(h, NP + g)));
+#pragma unroll
+                for (int h = 0; h < NQ; ++h)
 #pragma unroll
                     for (int r = 0; r < SLX; ++r) {
-                        const uint32_t cand = valid[r] & ~(P.k ? c2[r] : c0[r]);
+                        const uint32_t cand = valid[r] & ~(P.k ? c2[h][r] : c0[h][r]);
                         if (cand) {
-                            s_queue[qn * kSliceThreads + tid] = make_uint2(j | ((uint32_t)r << 16), cand);
+                            s_queue[qn * kSliceThreads + tid] = make_uint2((j + h) | ((uint32_t)r << 16), cand);
                             ++qn;
                         }
                     }
-                    if (__any_sync(0xffffffffu, qn > (uint32_t)(kSliceCap - SLX))) flush();
-                }
+                if (__any_sync(0xffffffffu, qn > (uint32_t)(kSliceCap - NQ * SLX))) flush();
             }
+#undef FPG_QS
+#undef FPG_QM
+#undef FPG_CNT
+        };
+        auto scan_queries = [&](auto slc) {
+            uint32_t j = 0;
+            if constexpr (NPT <= 48)  // query pairs while the registers allow it
+                for (; j + 2 <= tl.q_count; j += 2) step(slc, std::integral_constant<int, 2>{}, j);
+            for (; j < tl.q_count; ++j) step(slc, std::integral_constant<int, 1>{}, j);
         };
         if (SL == 2 && 32u * warp + kSliceThreads < tl.n_slabs) scan_queries(std::integral_constant<int, SL>{});
         else scan_queries(std::integral_constant<int, 1>{});
