@@ -47,6 +47,9 @@ struct Error : std::runtime_error {
 
 template <class F>
 int guarded(F&& f) {
+    // drop a non-sticky error left by an earlier failed call on this thread
+    // (e.g. cudaSetDevice on a bad ordinal), so it is not blamed on this one
+    (void)cudaGetLastError();
     try {
         f();
         return FPG_OK;
@@ -65,6 +68,7 @@ int guarded(F&& f) {
 inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 // per-run device counters: out_count, survivors, tile counter, candidates, big segment flag
 constexpr int kNumCounters = 5;
+constexpr unsigned kScatterBlocks = 148 * 4;  // grid-stride K4 scatter (the count is only known on the device)
 inline int stride_of(int len) { return len <= 16 ? 16 : (len + 15) & ~15; }
 
 // Device buffer that grows on demand (never shrinks), freed on destruction.
@@ -399,6 +403,7 @@ struct ShardBatch {
     std::vector<fpg::Tile> plan;
     std::vector<fpg::SliceTile> splan;
     bool plan_valid = false;
+    bool seg_k4 = true;  // speculative segmented K4 (reset at upload)
     fpg_query_options plan_opts{};
     DBuf<unsigned long long> out, sorted;
     DBuf<unsigned long long> counters;  // [0] out_count, [1] survivors_total, [2] tile counter
@@ -628,11 +633,12 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         const uint32_t qchunk = fpg::kSliceQ;
         auto add = [&](int lw, uint32_t qb, uint32_t qe, bool count_only) {
             const uint32_t ns = (uint32_t)cdiv(W.count[lw], 32);
+            const uint32_t per = chunk;
             for (uint32_t q0 = qb; q0 < qe; q0 += qchunk)
-                for (uint32_t s0 = 0; s0 < ns; s0 += chunk) {
+                for (uint32_t s0 = 0; s0 < ns; s0 += per) {
                     fpg::SliceTile t{};
                     t.slab_begin = s0;
-                    t.n_slabs = std::min(chunk, ns - s0);
+                    t.n_slabs = std::min(per, ns - s0);
                     t.q_begin = q0;
                     t.q_count = std::min<uint32_t>(qchunk, qe - q0);
                     t.plane_base = W.plane_base[lw];
@@ -770,8 +776,13 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         P.q_matches = S.qsurv.p + nq;
         P.big_seg = S.counters.p + 4;
     }
+    // K2, then K4 speculatively on the segmented path (no host round trip);
+    // the one sync reads the counters and redoes what they rule out: a
+    // larger output buffer (rescan) or a query with > kSegMax matches (CUB sort).
+    S.offsets.reserve(nq + 1);
     for (bool first = true;; first = false) {
         S.out.reserve(S.out_cap);
+        S.ids.reserve(S.out.cap);
         P.out = SP.out = S.out.p;
         P.out_cap = SP.out_cap = S.out.cap;
         if (!first) {  // rescan after growing the output (K1 zeroed them the first time)
@@ -787,6 +798,26 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
             ++S.launches;
         }
         CK(cudaEventRecord(S.ev[2], st));
+        // K4 (segmented): offsets = exclusive scan of the per-query match
+        // counts, keys scattered into their query's segment, one warp sorts
+        // each segment.  Skipped when this batch already showed large segments.
+        if (S.seg_k4 && nq) {
+            size_t tmp = 0;
+            CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, S.qsurv.p + nq, S.offsets.p, (int)nq, st));
+            S.cub_tmp.reserve(tmp);
+            CK(cub::DeviceScan::ExclusiveSum(S.cub_tmp.p, tmp, S.qsurv.p + nq, S.offsets.p, (int)nq, st));
+        }
+        if (S.seg_k4 || !nq) {
+            fpg::k_seg_scatter<<<kScatterBlocks, 256, 0, st>>>(S.out.p, S.counters.p, S.out.cap, S.offsets.p,
+                                                               S.qsurv.p + nq, S.ids.p, S.offsets.p + nq);
+            CK(cudaGetLastError());
+            ++S.launches;
+        }
+        if (S.seg_k4 && nq) {
+            fpg::k_seg_sort<<<(unsigned)cdiv(nq * 32, 256), 256, 0, st>>>(S.offsets.p, nq, S.out.cap, S.ids.p);
+            CK(cudaGetLastError());
+            S.launches += 2;
+        }
         CK(cudaMemcpyAsync(S.h_counters.p, S.counters.p, kNumCounters * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         if (S.h_counters.p[0] <= S.out.cap) break;
@@ -796,30 +827,15 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
     S.survivors = S.h_counters.p[1];
     S.candidates = S.h_counters.p[3];
 
-    // K4: order (query, word) keys and build the CSR.
-    S.sorted.reserve(S.total);
-    S.offsets.reserve(nq + 1);
-    S.ids.reserve(S.total);
-    int end_bit = 33;
-    while (end_bit < 64 && (1ull << (end_bit - 32)) <= nq) ++end_bit;
-    if (S.total && !S.h_counters.p[4]) {
-        // every query has <= kSegMax matches: offsets = exclusive scan of the
-        // per-query counts, keys scattered into their segments, one warp
-        // sorts each segment (no global sort, no further host round trip)
-        size_t tmp = 0;
-        CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, S.qsurv.p + nq, S.offsets.p, (int)nq, st));
-        S.cub_tmp.reserve(tmp);
-        CK(cub::DeviceScan::ExclusiveSum(S.cub_tmp.p, tmp, S.qsurv.p + nq, S.offsets.p, (int)nq, st));
-        fpg::k_seg_scatter<<<(unsigned)cdiv(S.total, 256), 256, 0, st>>>(S.out.p, S.counters.p, S.offsets.p,
-                                                                         S.qsurv.p + nq, nq, S.ids.p,
-                                                                         S.offsets.p + nq);
-        CK(cudaGetLastError());
-        fpg::k_seg_sort<<<(unsigned)cdiv(nq * 32, 256), 256, 0, st>>>(S.offsets.p, nq, S.ids.p);
-        CK(cudaGetLastError());
-        S.launches += 2;
-    } else if (!S.total) {
+    const bool seg_ran = S.seg_k4 || !nq;
+    if (S.h_counters.p[4]) S.seg_k4 = false;  // later runs of this batch go straight to the radix sort
+    if (!S.total && !seg_ran) {
         CK(cudaMemsetAsync(S.offsets.p, 0, (nq + 1) * sizeof(uint64_t), st));
-    } else {
+    } else if (S.total && (!seg_ran || S.h_counters.p[4])) {
+        // a query has more than kSegMax matches: order all keys with a radix sort
+        int end_bit = 33;
+        while (end_bit < 64 && (1ull << (end_bit - 32)) <= nq) ++end_bit;
+        S.sorted.reserve(S.total);
         size_t tmp = 0;
         CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, S.out.p, S.sorted.p, (int)S.total, 0, end_bit, st));
         S.cub_tmp.reserve(tmp);
@@ -912,6 +928,7 @@ void upload(fpg_batch* B, const uint8_t* qbytes, const uint64_t* qoffsets, uint6
         S.qoffs.reserve(nq + 1);
         S.qorder.reserve(nq);
         S.plan_valid = false;
+        S.seg_k4 = true;
         Collection& Q = S.queries;
         Q.n = nq;
         Q.count = B->qcount;

@@ -249,31 +249,54 @@ constexpr uint32_t kSegMax = 32;  // K4 warp-sorts segments up to this size
 
 // Match bookkeeping of one hit: per-query count (K4 segment size) and the
 // flag that routes K4 to the global radix sort when a segment is large.
-__device__ __forceinline__ void count_match(uint32_t* q_matches, unsigned long long* big_seg, uint32_t qid) {
-    if (atomicAdd(&q_matches[qid], 1u) == kSegMax) *big_seg = 1ull;
+// Called by the hit lanes of a warp (`hb` = ballot of hits, `head` = this
+// lane starts a run of adjacent hit lanes with the same query, `heads` = the
+// ballot of heads): one atomic per run, so popular queries do not serialise
+// on their counter.
+__device__ __forceinline__ void count_match(uint32_t* q_matches, unsigned long long* big_seg, uint32_t qid,
+                                            uint32_t hb, bool head, uint32_t heads) {
+    if (!head) return;
+    const int lane = threadIdx.x & 31;
+    const uint32_t above = heads & (0xfffffffeu << lane);  // later heads
+    const uint32_t upto = above ? ((1u << (__ffs(above) - 1)) - 1u) : 0xffffffffu;
+    const uint32_t n = (uint32_t)__popc(hb & upto & (0xffffffffu << lane));
+    const uint32_t old = atomicAdd(&q_matches[qid], n);
+    if (old <= kSegMax && old + n > kSegMax) *big_seg = 1ull;
+}
+
+// Run heads for count_match: a hit lane whose lower neighbour is not a hit
+// of the same query.  Warp-collective.
+__device__ __forceinline__ bool match_run_head(bool hit, uint32_t qid, uint32_t hb) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t prev = __shfl_up_sync(0xffffffffu, qid, 1);
+    return hit && (lane == 0 || !((hb >> (lane - 1)) & 1u) || prev != qid);
 }
 
 // K4 segmented (all segments <= kSegMax): keys -> their query's segment.
 __global__ void k_seg_scatter(const unsigned long long* __restrict__ keys, const unsigned long long* __restrict__ count,
-                              const uint64_t* __restrict__ offsets_in, uint32_t* __restrict__ cursor, uint64_t nq,
+                              uint64_t cap, const uint64_t* __restrict__ offsets_in, uint32_t* __restrict__ cursor,
                               uint32_t* __restrict__ ids, uint64_t* __restrict__ offsets_last) {
     const uint64_t total = *count;
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0) *offsets_last = total;
-    if (i >= total) return;
-    const unsigned long long k = keys[i];
-    const uint32_t q = (uint32_t)(k >> 32);
-    const uint32_t slot = atomicSub(&cursor[q], 1u) - 1u;
-    ids[offsets_in[q] + slot] = (uint32_t)k;
+    const uint64_t n = total < cap ? total : cap;  // overflowed runs are redone by the host
+    const uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i0 == 0) *offsets_last = total;
+    for (uint64_t i = i0; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long k = keys[i];
+        const uint32_t q = (uint32_t)(k >> 32);
+        const uint64_t pos = offsets_in[q] + (atomicSub(&cursor[q], 1u) - 1u);
+        if (pos < cap) ids[pos] = (uint32_t)k;
+    }
 }
 
 // One warp per query: bitonic sort of its <= 32 word ids in registers.
-__global__ void k_seg_sort(const uint64_t* __restrict__ offsets, uint64_t nq, uint32_t* __restrict__ ids) {
+__global__ void k_seg_sort(const uint64_t* __restrict__ offsets, uint64_t nq, uint64_t cap, uint32_t* __restrict__ ids) {
     const uint64_t q = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (q >= nq) return;
     const uint64_t o = offsets[q];
-    const int n = (int)(offsets[q + 1] - o);
+    const uint64_t e = offsets[q + 1];
+    if (e > cap || e - o > kSegMax) return;  // overflowed run / large segment: the host redoes K4
+    const int n = (int)(e - o);
     if (n <= 1) return;
     uint32_t v = lane < n ? ids[o + lane] : 0xffffffffu;
 #pragma unroll

@@ -274,14 +274,16 @@ struct TileScan {
                     unsigned long long slot = 0;
                     if (lane == 0) slot = atomicAdd(P.out_count, (unsigned long long)__popc(hb));
                     slot = __shfl_sync(0xffffffffu, slot, 0);
+                    const uint32_t qid = hit ? P.q_ids[tl.q_begin + j] : 0xffffffffu;
+                    const bool head = match_run_head(hit, qid, hb);
+                    const uint32_t heads = __ballot_sync(0xffffffffu, head);
                     if (hit) {
                         const uint64_t o = slot + __popc(hb & lt_mask);
                         if (o < P.out_cap) {
-                            const uint64_t qid = P.q_ids[tl.q_begin + j];
                             const uint64_t wid = P.id_base + P.w_ids[tl.w_begin + widx];
-                            P.out[o] = (qid << 32) | wid;
+                            P.out[o] = ((uint64_t)qid << 32) | wid;
                         }
-                        count_match(P.q_matches, P.big_seg, P.q_ids[tl.q_begin + j]);
+                        count_match(P.q_matches, P.big_seg, qid, hb, head, heads);
                     }
                 }
             }

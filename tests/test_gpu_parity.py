@@ -227,6 +227,25 @@ def test_output_regrowth_many_matches(oracle):
     assert_same(csr, st, *oracle.query_batch(blob, offs, qblob, qoffs, osch(s), Metric.Levenshtein, 1, True, True))
 
 
+def test_staged_batch_reruns_across_options(oracle):
+    """One upload, several runs (fpg_batch_run) with options whose outputs
+    differ in size and shape: the cached tile plan and the K4 path choice
+    (segmented vs radix sort, chosen per batch) must follow the options."""
+    blob, offs = generate_dictionary(3, n=60_000)
+    pats = [b"e", b"ea", b"th"] * 3
+    qb2, qo2 = generate_queries(3, blob, offs, nq=200)
+    qblob, qoffs = pack(pats + [bytes(qb2[int(qo2[i]):int(qo2[i + 1])]) for i in range(200)])
+    s = make_scheme(blob, Variant.Occurrence, 16)
+    with GpuFingerprintedDictionary((blob, offs), s) as d:
+        b = d.batch()
+        b.upload(qblob, qoffs)
+        for metric, k, pre in [(Metric.Levenshtein, 1, True), (Metric.Hamming, 0, True),
+                               (Metric.Levenshtein, 1, False), (Metric.Hamming, 1, True), (Metric.Levenshtein, 0, True)]:
+            b.run(QueryOptions(metric, k, True, pre), want_stats=True)
+            csr, st = b.download()
+            assert_same(csr, st, *oracle.query_batch(blob, offs, qblob, qoffs, osch(s), metric, k, True, pre))
+
+
 @pytest.mark.slow
 def test_config2_full_dictionary_subsample(oracle):
     """Full config 2 (1e6 words, 10,000 queries) on the GPU; every 10th query
