@@ -182,7 +182,12 @@ bool supports(int variant, int metric) {
     return metric == FPG_HAMMING || variant == FPG_OCCURRENCE || variant == FPG_COUNT;
 }
 
-uint64_t g_launches = 0;  // approximate, per process; per-run counts are exact below
+uint64_t g_launches = 0;
+
+double env_double(const char* name, double dflt) {
+    const char* e = std::getenv(name);
+    return e && *e ? std::atof(e) : dflt;
+}  // approximate, per process; per-run counts are exact below
 
 // The verifier's occurrence-signature pre-check (exact; see occurrence_sig)
 // can be switched off with FPG_SIG_PRECHECK=0 to compare both paths.
@@ -673,16 +678,18 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         for (const auto& t : splan) work += cost(t);
         std::vector<fpg::SliceTile> fine;
         fine.reserve(splan.size() + splan.size() / 2);
+        static const double tail_a = env_double("FPG_TAIL_A", 0.35), tail_b = env_double("FPG_TAIL_B", 0.85);
         for (const auto& t : splan) {
             acc += cost(t);
-            if (acc * 10 <= work * 7 || t.q_count <= 32) {
+            const uint32_t sub = acc <= tail_a * work ? t.q_count : acc <= tail_b * work ? 32u : 16u;
+            if (t.q_count <= sub) {
                 fine.push_back(t);
                 continue;
             }
-            for (uint32_t q0 = 0; q0 < t.q_count; q0 += 32) {
+            for (uint32_t q0 = 0; q0 < t.q_count; q0 += sub) {
                 fpg::SliceTile u = t;
                 u.q_begin = t.q_begin + q0;
-                u.q_count = std::min<uint32_t>(32, t.q_count - q0);
+                u.q_count = std::min<uint32_t>(sub, t.q_count - q0);
                 fine.push_back(u);
             }
         }
