@@ -184,6 +184,11 @@ bool supports(int variant, int metric) {
 
 uint64_t g_launches = 0;
 
+const bool g_trace = [] {
+    const char* e = std::getenv("FPG_TRACE");
+    return e && e[0] == '1';
+}();
+
 double env_double(const char* name, double dflt) {
     const char* e = std::getenv(name);
     return e && *e ? std::atof(e) : dflt;
@@ -408,6 +413,7 @@ struct ShardBatch {
     std::vector<fpg::Tile> plan;
     std::vector<fpg::SliceTile> splan;
     bool plan_valid = false;
+    std::vector<uint32_t> plan_qcount;  // query length histogram the plan was built for
     bool seg_k4 = true;  // speculative segmented K4 (reset at upload)
     fpg_query_options plan_opts{};
     DBuf<unsigned long long> out, sorted;
@@ -621,8 +627,9 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
     uint64_t executed = 0;
     std::vector<fpg::Tile>& plan = S.plan;
     std::vector<fpg::SliceTile>& splan = S.splan;
-    // The tile plan depends only on the uploaded batch and the options: it is
-    // built (and uploaded) on the first run of a batch and reused after.
+    // The tile plan depends only on the batch's length histogram and the
+    // options: it is built (and uploaded) once and reused by later runs and
+    // by later batches with the same histogram.
     const bool replan = !S.plan_valid || std::memcmp(&S.plan_opts, &o, sizeof(o)) != 0;
     if (!replan) {
         executed = S.executed;
@@ -888,6 +895,7 @@ void check_opts(const fpg_dict* D, const fpg_query_options* o) {
 }
 
 void upload(fpg_batch* B, const uint8_t* qbytes, const uint64_t* qoffsets, uint64_t nq) {
+    const auto t0 = std::chrono::steady_clock::now();
     if (nq && !qoffsets) throw Error(FPG_EINVAL, "null query offsets");
     if (nq >= (1ull << 31)) throw Error(FPG_EINVAL, "too many queries in one batch");
     B->nq = nq;
@@ -927,6 +935,7 @@ void upload(fpg_batch* B, const uint8_t* qbytes, const uint64_t* qoffsets, uint6
         for (uint64_t i = 0; i < nq; ++i) B->h_order.p[cur[B->qlen[i]]++] = (uint32_t)i;
     }
     const uint64_t nbytes = nq ? qoffsets[nq] - q0 : 0;
+    const auto t1 = std::chrono::steady_clock::now();
     for_each_shard(B->sb.size(), [&](size_t i) {
         ShardBatch& S = *B->sb[i];
         CK(cudaSetDevice(S.sh->device));
@@ -934,7 +943,13 @@ void upload(fpg_batch* B, const uint8_t* qbytes, const uint64_t* qoffsets, uint6
         S.qblob.reserve(nbytes + 16);
         S.qoffs.reserve(nq + 1);
         S.qorder.reserve(nq);
-        S.plan_valid = false;
+        // the tile plan and the bucket tables depend on the batch only
+        // through its length histogram
+        const bool new_hist = S.plan_qcount != B->qcount;
+        if (new_hist) {
+            S.plan_valid = false;
+            S.plan_qcount = B->qcount;
+        }
         S.seg_k4 = true;
         Collection& Q = S.queries;
         Q.n = nq;
@@ -956,10 +971,18 @@ void upload(fpg_batch* B, const uint8_t* qbytes, const uint64_t* qoffsets, uint6
                 CK(cudaMemcpyAsync(S.qoffs.p, rebased.data(), (nq + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
             }
         }
-        CK(cudaMemcpyAsync(Q.d_start.p, B->h_start.p, L1 * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(Q.d_byte_base.p, B->h_bbase.p, L1 * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+        if (new_hist) {
+            CK(cudaMemcpyAsync(Q.d_start.p, B->h_start.p, L1 * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(Q.d_byte_base.p, B->h_bbase.p, L1 * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+        }
         CK(cudaStreamSynchronize(st));  // caller buffers may be reused once upload returns
     });
+    if (g_trace) {
+        const auto t2 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "fpg upload: host bucketing %.1f us, h2d %.1f us\n",
+                     std::chrono::duration<double, std::micro>(t1 - t0).count(),
+                     std::chrono::duration<double, std::micro>(t2 - t1).count());
+    }
 }
 
 void run(fpg_batch* B, const fpg_query_options* o) {
@@ -974,7 +997,9 @@ void download(fpg_batch* B, fpg_result* out) {
     if (!B->ran) throw Error(FPG_EINVAL, "fpg_batch_download before fpg_batch_run");
     const fpg_query_options& o = B->opt;
     const bool stats = o.want_stats != 0;
+    const auto t0 = std::chrono::steady_clock::now();
     for_each_shard(B->sb.size(), [&](size_t i) { download_shard(B, *B->sb[i], stats); });
+    const auto t1 = std::chrono::steady_clock::now();
     const uint64_t nq = B->nq;
     std::memset(out, 0, sizeof(*out));
     out->nq = nq;
@@ -1030,6 +1055,12 @@ void download(fpg_batch* B, fpg_result* out) {
             st[FPG_STAT_REJECTED_BY_FINGERPRINT] = comp - verified;
             st[FPG_STAT_MATCHES] = out->offsets[q + 1] - out->offsets[q];
         }
+    }
+    if (g_trace) {
+        const auto t2 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "fpg download: d2h %.1f us, assemble %.1f us\n",
+                     std::chrono::duration<double, std::micro>(t1 - t0).count(),
+                     std::chrono::duration<double, std::micro>(t2 - t1).count());
     }
 }
 

@@ -343,15 +343,18 @@ class MatchCSR:
 
 
 def _take_result(res: FpgResult, want_stats: bool):
+    """Copies the library-owned CSR (and stats) into numpy arrays, then frees it."""
     nq, total = int(res.nq), int(res.total)
-    offsets = np.ctypeslib.as_array(res.offsets, shape=(nq + 1,)).copy()
-    ids = (np.ctypeslib.as_array(res.word_ids, shape=(total,)).copy() if total
-           else np.zeros(0, np.uint32))
-    stats = None
-    if want_stats and nq:
-        stats = np.ctypeslib.as_array(res.stats, shape=(nq, 5)).copy()
-    elif want_stats:
-        stats = np.zeros((0, 5), np.uint64)
+
+    def take(p, n, dtype):
+        out = np.empty(n, dtype=dtype)
+        if n:
+            ctypes.memmove(out.ctypes.data, ctypes.cast(p, ctypes.c_void_p).value, out.nbytes)
+        return out
+
+    offsets = take(res.offsets, nq + 1, np.uint64)
+    ids = take(res.word_ids, total, np.uint32)
+    stats = take(res.stats, nq * 5, np.uint64).reshape(nq, 5) if want_stats else None
     check(load_fpg().fpg_result_free(ctypes.byref(res)))
     return MatchCSR(offsets, ids), stats
 
