@@ -24,6 +24,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 
 #include "../../include/fpg.h"
 #include "fpg_kernels.cuh"
@@ -416,11 +417,12 @@ struct ShardBatch {
     std::vector<uint32_t> plan_qcount;  // query length histogram the plan was built for
     bool seg_k4 = true;  // speculative segmented K4 (reset at upload)
     fpg_query_options plan_opts{};
-    DBuf<unsigned long long> out, sorted;
+    DBuf<unsigned long long> out;
     DBuf<unsigned long long> counters;  // [0] out_count, [1] survivors_total, [2] tile counter
     DBuf<uint32_t> qsurv;
     DBuf<uint64_t> offsets;
-    DBuf<uint32_t> ids;
+    DBuf<uint32_t> ids, ids2;
+    const uint32_t* ids_out = nullptr;  // sorted word ids of the last run (ids or ids2)
     DBuf<uint8_t> cub_tmp;
     HBuf<unsigned long long> h_counters;
     HBuf<uint64_t> h_offsets;
@@ -812,25 +814,24 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
             ++S.launches;
         }
         CK(cudaEventRecord(S.ev[2], st));
-        // K4 (segmented): offsets = exclusive scan of the per-query match
-        // counts, keys scattered into their query's segment, one warp sorts
-        // each segment.  Skipped when this batch already showed large segments.
-        if (S.seg_k4 && nq) {
+        // K4: offsets = exclusive scan of the per-query match counts, keys
+        // scattered into their query's segment, then each segment sorted by
+        // one warp (<= kSegMax matches).  Batches known to have larger
+        // segments skip the warp sort; the host sorts their segments below.
+        if (nq) {
             size_t tmp = 0;
             CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, S.qsurv.p + nq, S.offsets.p, (int)nq, st));
             S.cub_tmp.reserve(tmp);
             CK(cub::DeviceScan::ExclusiveSum(S.cub_tmp.p, tmp, S.qsurv.p + nq, S.offsets.p, (int)nq, st));
         }
-        if (S.seg_k4 || !nq) {
-            fpg::k_seg_scatter<<<kScatterBlocks, 256, 0, st>>>(S.out.p, S.counters.p, S.out.cap, S.offsets.p,
-                                                               S.qsurv.p + nq, S.ids.p, S.offsets.p + nq);
-            CK(cudaGetLastError());
-            ++S.launches;
-        }
+        fpg::k_seg_scatter<<<kScatterBlocks, 256, 0, st>>>(S.out.p, S.counters.p, S.out.cap, S.offsets.p,
+                                                           S.qsurv.p + nq, S.ids.p, S.offsets.p + nq);
+        CK(cudaGetLastError());
+        S.launches += 2;
         if (S.seg_k4 && nq) {
             fpg::k_seg_sort<<<(unsigned)cdiv(nq * 32, 256), 256, 0, st>>>(S.offsets.p, nq, S.out.cap, S.ids.p);
             CK(cudaGetLastError());
-            S.launches += 2;
+            ++S.launches;
         }
         CK(cudaMemcpyAsync(S.h_counters.p, S.counters.p, kNumCounters * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
@@ -841,24 +842,21 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
     S.survivors = S.h_counters.p[1];
     S.candidates = S.h_counters.p[3];
 
-    const bool seg_ran = S.seg_k4 || !nq;
-    if (S.h_counters.p[4]) S.seg_k4 = false;  // later runs of this batch go straight to the radix sort
-    if (!S.total && !seg_ran) {
-        CK(cudaMemsetAsync(S.offsets.p, 0, (nq + 1) * sizeof(uint64_t), st));
-    } else if (S.total && (!seg_ran || S.h_counters.p[4])) {
-        // a query has more than kSegMax matches: order all keys with a radix sort
-        int end_bit = 33;
-        while (end_bit < 64 && (1ull << (end_bit - 32)) <= nq) ++end_bit;
-        S.sorted.reserve(S.total);
+    S.ids_out = S.ids.p;
+    if (S.h_counters.p[4] && S.total) {
+        // some query has more than kSegMax matches: sort every segment (CUB
+        // segmented sort of the 32-bit word ids; later runs of this batch
+        // skip the warp sort)
+        S.seg_k4 = false;
+        S.ids2.reserve(S.total);
         size_t tmp = 0;
-        CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, S.out.p, S.sorted.p, (int)S.total, 0, end_bit, st));
+        CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, S.ids.p, S.ids2.p, (int)S.total, (int)nq, S.offsets.p,
+                                              S.offsets.p + 1, st));
         S.cub_tmp.reserve(tmp);
-        CK(cub::DeviceRadixSort::SortKeys(S.cub_tmp.p, tmp, S.out.p, S.sorted.p, (int)S.total, 0, end_bit, st));
-        fpg::k_low_ids<<<(unsigned)cdiv(S.total, 256), 256, 0, st>>>(S.sorted.p, S.total, S.ids.p);
-        CK(cudaGetLastError());
-        fpg::k_offsets<<<(unsigned)cdiv(nq + 1, 256), 256, 0, st>>>(S.sorted.p, S.total, nq, S.offsets.p);
-        CK(cudaGetLastError());
-        S.launches += 2;
+        CK(cub::DeviceSegmentedSort::SortKeys(S.cub_tmp.p, tmp, S.ids.p, S.ids2.p, (int)S.total, (int)nq,
+                                              S.offsets.p, S.offsets.p + 1, st));
+        S.ids_out = S.ids2.p;
+        ++S.launches;
     }
     CK(cudaEventRecord(S.ev[3], st));
     CK(cudaEventSynchronize(S.ev[3]));
@@ -877,7 +875,7 @@ void download_shard(fpg_batch* B, ShardBatch& S, bool stats) {
     S.h_offsets.reserve(nq + 1);
     S.h_ids.reserve(S.total);
     CK(cudaMemcpyAsync(S.h_offsets.p, S.offsets.p, (nq + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-    if (S.total) CK(cudaMemcpyAsync(S.h_ids.p, S.ids.p, S.total * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    if (S.total) CK(cudaMemcpyAsync(S.h_ids.p, S.ids_out, S.total * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     if (stats && nq) {
         S.h_qsurv.reserve(nq);
         CK(cudaMemcpyAsync(S.h_qsurv.p, S.qsurv.p, nq * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));

@@ -10,7 +10,9 @@
 //                   compacted per warp with __ballot_sync into shared memory
 //                   and verified there at k<=1 (edit_distance.hpp:18-64),
 //                   matches appended with warp-aggregated atomics.
-//   K4 k_offsets / k_low_ids   CSR of the radix-sorted (query, word) keys.
+//   K4 k_seg_scatter / k_seg_sort   CSR: keys scattered into per-query
+//                   segments, small segments warp-sorted (large ones: CUB
+//                   segmented sort on the host side of the launch).
 #pragma once
 
 #include <cstdint>
@@ -224,27 +226,6 @@ __global__ void k_scatter_prints(const uint64_t* __restrict__ fp, const uint32_t
 }
 
 // ---------------------------------------------------------------- K4 CSR
-// offsets[q] = lower_bound(keys, q << 32) for q in [0, nq]; keys sorted.
-__global__ void k_offsets(const unsigned long long* __restrict__ keys, uint64_t total, uint64_t nq,
-                          uint64_t* __restrict__ offsets) {
-    const uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q > nq) return;
-    const unsigned long long key = (unsigned long long)q << 32;
-    uint64_t lo = 0, hi = total;
-    while (lo < hi) {
-        const uint64_t mid = (lo + hi) >> 1;
-        if (keys[mid] < key) lo = mid + 1;
-        else hi = mid;
-    }
-    offsets[q] = lo;
-}
-
-__global__ void k_low_ids(const unsigned long long* __restrict__ keys, uint64_t total,
-                          uint32_t* __restrict__ ids) {
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < total) ids[i] = (uint32_t)keys[i];
-}
-
 constexpr uint32_t kSegMax = 32;  // K4 warp-sorts segments up to this size
 
 // Match bookkeeping of one hit: per-query count (K4 segment size) and the
