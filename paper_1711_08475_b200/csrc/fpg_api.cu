@@ -67,8 +67,9 @@ int guarded(F&& f) {
 }
 
 inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
-// per-run device counters: out_count, survivors, tile counter, candidates, big segment flag
-constexpr int kNumCounters = 5;
+// per-run device counters: key slots reserved, survivors, tile counter, verifier
+// candidates, big segment flag, matches
+constexpr int kNumCounters = 6;
 constexpr unsigned kScatterBlocks = 148 * 4;  // grid-stride K4 scatter (the count is only known on the device)
 inline int stride_of(int len) { return len <= 16 ? 16 : (len + 15) & ~15; }
 
@@ -764,7 +765,7 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         SP.tile_counter = reinterpret_cast<unsigned int*>(S.counters.p + 2);
         SP.candidates = S.counters.p + 3;
         SP.q_matches = S.qsurv.p + nq;
-        SP.big_seg = S.counters.p + 4;
+        SP.match_total = S.counters.p + 5;
         SP.k = o.k;
         SP.stats = (o.want_stats && o.use_filter) ? 1 : 0;
         SP.use_fp = supports(D->scheme.variant, o.metric) ? 1 : 0;
@@ -790,12 +791,13 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         P.fold = D->params.variant == FPG_COUNT ? D->params.b
                : D->params.variant == FPG_POSITION ? D->params.p : 1;
         P.q_matches = S.qsurv.p + nq;
-        P.big_seg = S.counters.p + 4;
+        P.match_total = S.counters.p + 5;
     }
     // K2, then K4 speculatively on the segmented path (no host round trip);
     // the one sync reads the counters and redoes what they rule out: a
     // larger output buffer (rescan) or a query with > kSegMax matches (CUB sort).
     S.offsets.reserve(nq + 1);
+    const bool warp_sort = S.seg_k4 && nq;  // this run warp-sorts the segments (else CUB below)
     for (bool first = true;; first = false) {
         S.out.reserve(S.out_cap);
         S.ids.reserve(S.out.cap);
@@ -824,26 +826,27 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
             S.cub_tmp.reserve(tmp);
             CK(cub::DeviceScan::ExclusiveSum(S.cub_tmp.p, tmp, S.qsurv.p + nq, S.offsets.p, (int)nq, st));
         }
-        fpg::k_seg_scatter<<<kScatterBlocks, 256, 0, st>>>(S.out.p, S.counters.p, S.out.cap, S.offsets.p,
-                                                           S.qsurv.p + nq, S.ids.p, S.offsets.p + nq);
+        fpg::k_seg_scatter<<<kScatterBlocks, 256, 0, st>>>(S.out.p, S.counters.p, S.counters.p + 5, S.out.cap,
+                                                           S.offsets.p, S.qsurv.p + nq, S.ids.p, S.offsets.p + nq);
         CK(cudaGetLastError());
         S.launches += 2;
-        if (S.seg_k4 && nq) {
-            fpg::k_seg_sort<<<(unsigned)cdiv(nq * 32, 256), 256, 0, st>>>(S.offsets.p, nq, S.out.cap, S.ids.p);
+        if (warp_sort) {
+            fpg::k_seg_sort<<<(unsigned)cdiv(nq * 32, 256), 256, 0, st>>>(S.offsets.p, nq, S.out.cap, S.ids.p,
+                                                                           S.counters.p + 4);
             CK(cudaGetLastError());
             ++S.launches;
         }
         CK(cudaMemcpyAsync(S.h_counters.p, S.counters.p, kNumCounters * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        if (S.h_counters.p[0] <= S.out.cap) break;
+        if (S.h_counters.p[0] <= S.out.cap) break;  // reserved key slots fit
         S.out_cap = S.h_counters.p[0] + S.h_counters.p[0] / 4 + 1024;  // grow and rescan
     }
-    S.total = S.h_counters.p[0];
+    S.total = S.h_counters.p[5];
     S.survivors = S.h_counters.p[1];
     S.candidates = S.h_counters.p[3];
 
     S.ids_out = S.ids.p;
-    if (S.h_counters.p[4] && S.total) {
+    if (S.total && (!warp_sort || S.h_counters.p[4])) {
         // some query has more than kSegMax matches: sort every segment (CUB
         // segmented sort of the 32-bit word ids; later runs of this batch
         // skip the warp sort)

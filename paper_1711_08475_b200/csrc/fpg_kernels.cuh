@@ -56,7 +56,8 @@ struct ScanParams {
     uint64_t id_base;           // added to word ids
     uint32_t* q_survivors;      // per input query: pairs passing the fingerprint test
     unsigned long long* out;    // (query << 32 | word) match keys
-    unsigned long long* out_count;
+    unsigned long long* out_count;  // key slots reserved (OutChunk)
+    unsigned long long* match_total;
     unsigned long long* survivors_total;
     uint64_t out_cap;
     uint64_t mask_fold, mask_single;
@@ -66,7 +67,6 @@ struct ScanParams {
     const uint32_t* q_sig;      // occurrence signatures (verifier pre-check)
     const uint32_t* w_sig;
     uint32_t* q_matches;        // per input query: matches (K4 segment sizes)
-    unsigned long long* big_seg;  // set when a query exceeds kSegMax matches
 };
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
@@ -228,22 +228,55 @@ __global__ void k_scatter_prints(const uint64_t* __restrict__ fp, const uint32_t
 // ---------------------------------------------------------------- K4 CSR
 constexpr uint32_t kSegMax = 32;  // K4 warp-sorts segments up to this size
 
-// Match bookkeeping of one hit: per-query count (K4 segment size) and the
-// flag that routes K4 to the global radix sort when a segment is large.
+// Match bookkeeping of one hit: per-query count (the K4 segment size).
 // Called by the hit lanes of a warp (`hb` = ballot of hits, `head` = this
 // lane starts a run of adjacent hit lanes with the same query, `heads` = the
-// ballot of heads): one atomic per run, so popular queries do not serialise
-// on their counter.
-__device__ __forceinline__ void count_match(uint32_t* q_matches, unsigned long long* big_seg, uint32_t qid,
-                                            uint32_t hb, bool head, uint32_t heads) {
+// ballot of heads): one fire-and-forget reduction per run, so popular queries
+// do not serialise on their counter.  Large segments are detected in K4.
+__device__ __forceinline__ void count_match(uint32_t* q_matches, uint32_t qid, uint32_t hb, bool head,
+                                            uint32_t heads) {
     if (!head) return;
     const int lane = threadIdx.x & 31;
     const uint32_t above = heads & (0xfffffffeu << lane);  // later heads
     const uint32_t upto = above ? ((1u << (__ffs(above) - 1)) - 1u) : 0xffffffffu;
-    const uint32_t n = (uint32_t)__popc(hb & upto & (0xffffffffu << lane));
-    const uint32_t old = atomicAdd(&q_matches[qid], n);
-    if (old <= kSegMax && old + n > kSegMax) *big_seg = 1ull;
+    atomicAdd(&q_matches[qid], (uint32_t)__popc(hb & upto & (0xffffffffu << lane)));
 }
+
+// Per-warp output chunk: a warp reserves kOutChunk key slots with one atomic
+// and fills them over many ballots; slots it leaves unused hold kNoKey (K4
+// skips them).  Keeps the global slot counter out of the per-hit path.
+constexpr uint32_t kOutChunk = 64;
+constexpr unsigned long long kNoKey = ~0ull;
+
+struct OutChunk {
+    uint64_t base = ~0ull;  // first slot of the current chunk (warp-uniform)
+    uint32_t fill = kOutChunk;
+    uint32_t real = 0;      // hits emitted by this warp
+
+    __device__ __forceinline__ void close(unsigned long long* out, uint64_t cap) {
+        if (base == ~0ull) return;
+        for (uint32_t i = fill + (threadIdx.x & 31); i < kOutChunk; i += 32)
+            if (base + i < cap) out[base + i] = kNoKey;
+    }
+    // Warp-collective: `hit` lanes append `key`.
+    __device__ __forceinline__ void emit(uint32_t hb, bool hit, unsigned long long key, unsigned long long* out,
+                                         uint64_t cap, unsigned long long* slots) {
+        const uint32_t h = (uint32_t)__popc(hb);
+        if (fill + h > kOutChunk) {
+            close(out, cap);
+            unsigned long long b = 0;
+            if ((threadIdx.x & 31) == 0) b = atomicAdd(slots, (unsigned long long)kOutChunk);
+            base = __shfl_sync(0xffffffffu, b, 0);
+            fill = 0;
+        }
+        if (hit) {
+            const uint64_t o = base + fill + (uint32_t)__popc(hb & ((1u << (threadIdx.x & 31)) - 1u));
+            if (o < cap) out[o] = key;
+        }
+        fill += h;
+        real += h;
+    }
+};
 
 // Run heads for count_match: a hit lane whose lower neighbour is not a hit
 // of the same query.  Warp-collective.
@@ -254,15 +287,17 @@ __device__ __forceinline__ bool match_run_head(bool hit, uint32_t qid, uint32_t 
 }
 
 // K4 segmented (all segments <= kSegMax): keys -> their query's segment.
-__global__ void k_seg_scatter(const unsigned long long* __restrict__ keys, const unsigned long long* __restrict__ count,
-                              uint64_t cap, const uint64_t* __restrict__ offsets_in, uint32_t* __restrict__ cursor,
+__global__ void k_seg_scatter(const unsigned long long* __restrict__ keys, const unsigned long long* __restrict__ slots,
+                              const unsigned long long* __restrict__ matches, uint64_t cap,
+                              const uint64_t* __restrict__ offsets_in, uint32_t* __restrict__ cursor,
                               uint32_t* __restrict__ ids, uint64_t* __restrict__ offsets_last) {
-    const uint64_t total = *count;
-    const uint64_t n = total < cap ? total : cap;  // overflowed runs are redone by the host
+    const uint64_t used = *slots;
+    const uint64_t n = used < cap ? used : cap;  // overflowed runs are redone by the host
     const uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i0 == 0) *offsets_last = total;
+    if (i0 == 0) *offsets_last = *matches;
     for (uint64_t i = i0; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const unsigned long long k = keys[i];
+        if (k == kNoKey) continue;
         const uint32_t q = (uint32_t)(k >> 32);
         const uint64_t pos = offsets_in[q] + (atomicSub(&cursor[q], 1u) - 1u);
         if (pos < cap) ids[pos] = (uint32_t)k;
@@ -270,13 +305,18 @@ __global__ void k_seg_scatter(const unsigned long long* __restrict__ keys, const
 }
 
 // One warp per query: bitonic sort of its <= 32 word ids in registers.
-__global__ void k_seg_sort(const uint64_t* __restrict__ offsets, uint64_t nq, uint64_t cap, uint32_t* __restrict__ ids) {
+__global__ void k_seg_sort(const uint64_t* __restrict__ offsets, uint64_t nq, uint64_t cap, uint32_t* __restrict__ ids,
+                           unsigned long long* __restrict__ big_seg) {
     const uint64_t q = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (q >= nq) return;
     const uint64_t o = offsets[q];
     const uint64_t e = offsets[q + 1];
-    if (e > cap || e - o > kSegMax) return;  // overflowed run / large segment: the host redoes K4
+    if (e - o > kSegMax) {  // large segment: the host sorts all segments (CUB)
+        if (lane == 0) *big_seg = 1ull;
+        return;
+    }
+    if (e > cap) return;  // overflowed run: the host reruns
     const int n = (int)(e - o);
     if (n <= 1) return;
     uint32_t v = lane < n ? ids[o + lane] : 0xffffffffu;

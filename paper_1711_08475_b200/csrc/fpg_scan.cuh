@@ -225,6 +225,7 @@ struct TileScan {
     uint32_t a_qlimit;   // flush once qp passes the last slot
     uint32_t a_qsig;
     uint32_t qp;
+    OutChunk& oc;
 
     __device__ __forceinline__ bool verify_bytes(uint32_t j, uint32_t widx) const {
         const uint8_t* qb = qbytes + (uint64_t)j * qs;
@@ -249,7 +250,6 @@ struct TileScan {
     // fingerprint and the signature test (rare: each lane walks its own bits).
     __device__ __forceinline__ void flush() {
         __syncwarp();
-        const uint32_t lt_mask = (1u << lane) - 1u;
         const int cnt = (int)((qp - a_queue) >> 7);
         const int maxc = (int)__reduce_max_sync(0xffffffffu, (unsigned)cnt);
         for (int s = 0; s < maxc; ++s) {
@@ -271,20 +271,12 @@ struct TileScan {
                 }
                 const uint32_t hb = __ballot_sync(0xffffffffu, hit);
                 if (hb) {
-                    unsigned long long slot = 0;
-                    if (lane == 0) slot = atomicAdd(P.out_count, (unsigned long long)__popc(hb));
-                    slot = __shfl_sync(0xffffffffu, slot, 0);
                     const uint32_t qid = hit ? P.q_ids[tl.q_begin + j] : 0xffffffffu;
                     const bool head = match_run_head(hit, qid, hb);
                     const uint32_t heads = __ballot_sync(0xffffffffu, head);
-                    if (hit) {
-                        const uint64_t o = slot + __popc(hb & lt_mask);
-                        if (o < P.out_cap) {
-                            const uint64_t wid = P.id_base + P.w_ids[tl.w_begin + widx];
-                            P.out[o] = ((uint64_t)qid << 32) | wid;
-                        }
-                        count_match(P.q_matches, P.big_seg, qid, hb, head, heads);
-                    }
+                    const uint64_t wid = hit ? P.id_base + P.w_ids[tl.w_begin + widx] : 0;
+                    oc.emit(hb, hit, ((uint64_t)qid << 32) | wid, P.out, P.out_cap, P.out_count);
+                    if (hit) count_match(P.q_matches, qid, hb, head, heads);
                 }
             }
         }
@@ -373,6 +365,7 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(const Tile* __restrict
     const uint32_t a_q = smem_u32(s_q), a_qsig = smem_u32(s_qsig);
     const uint32_t a_wsurv = smem_u32(s_wsurv + (STATS ? warp * kTileQueries : 0));
     unsigned long long surv_warp = 0;  // lane 0's copy is the warp total (STATS)
+    OutChunk oc;
 
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const Tile tl = tiles[t];
@@ -399,7 +392,7 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(const Tile* __restrict
             TileScan<KIND, T, STATS> ts{P, tl, P.q_bytes + tl.q_bytes, P.w_bytes + tl.w_bytes,
                                         tl.q_len, tl.w_len, tl.q_stride, tl.w_stride,
                                         (tl.q_len <= 16 && tl.w_len <= 16) ? 1 : (tl.q_len <= 32 && tl.w_len <= 32) ? 2 : 0,
-                                        tid, lane, a_queue, a_queue + 128u * (kLaneCap - 1), a_qsig, a_queue};
+                                        tid, lane, a_queue, a_queue + 128u * (kLaneCap - 1), a_qsig, a_queue, oc};
             surv_warp += ts.scan(a_q, wc, wg, vmask, a_wsurv);
         } else if constexpr (STATS) {
             // incompatible lengths with the length prefilter off: the reference
@@ -430,6 +423,8 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(const Tile* __restrict
     }
     // run total of fingerprint survivors (reported), one atomic per warp
     if (STATS && lane == 0 && surv_warp) atomicAdd(P.survivors_total, surv_warp);
+    oc.close(P.out, P.out_cap);
+    if (lane == 0 && oc.real) atomicAdd(P.match_total, (unsigned long long)oc.real);
 }
 
 // Dynamic shared memory of k_scan<.., W, STATS>.

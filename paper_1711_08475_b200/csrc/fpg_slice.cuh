@@ -82,12 +82,12 @@ struct SliceParams {
     uint64_t id_base;
     uint32_t* q_survivors;
     unsigned long long* out;
-    unsigned long long* out_count;
+    unsigned long long* out_count;    // key slots reserved (OutChunk)
+    unsigned long long* match_total;
     unsigned long long* survivors_total;
     unsigned int* tile_counter;
     unsigned long long* candidates;  // pairs handed to the byte verifier
     uint32_t* q_matches;             // per input query: matches (K4 segment sizes)
-    unsigned long long* big_seg;
     uint64_t out_cap;
     int32_t k;
     int32_t stats;
@@ -129,9 +129,9 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
     __shared__ uint32_t s_next[2];  // next tile index, double-buffered by iteration parity
     __shared__ uint32_t s_surv[kSliceQ];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t lt_mask = (1u << lane) - 1u;
     unsigned long long surv_warp = 0;  // lane 0: the warp's fingerprint survivors
     uint32_t cand_lane = 0;
+    OutChunk oc;
 
     if (tid == 0) s_next[0] = atomicAdd(P.tile_counter, 1u);
     __syncthreads();
@@ -251,20 +251,12 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                     }
                     const uint32_t hb = __ballot_sync(0xffffffffu, hit);
                     if (hb) {
-                        unsigned long long slot = 0;
-                        if (lane == 0) slot = atomicAdd(P.out_count, (unsigned long long)__popc(hb));
-                        slot = __shfl_sync(0xffffffffu, slot, 0);
                         const uint32_t qid = s_qid[j];
                         const bool head = match_run_head(hit, qid, hb);
                         const uint32_t heads = __ballot_sync(0xffffffffu, head);
-                        if (hit) {
-                            const uint64_t o = slot + __popc(hb & lt_mask);
-                            if (o < P.out_cap) {
-                                const uint64_t wid = P.id_base + P.w_ids[tl.w_start + widx];
-                                P.out[o] = ((uint64_t)qid << 32) | wid;
-                            }
-                            count_match(P.q_matches, P.big_seg, qid, hb, head, heads);
-                        }
+                        const uint64_t wid = hit ? P.id_base + P.w_ids[tl.w_start + widx] : 0;
+                        oc.emit(hb, hit, ((uint64_t)qid << 32) | wid, P.out, P.out_cap, P.out_count);
+                        if (hit) count_match(P.q_matches, qid, hb, head, heads);
                     }
                 }
                 __syncwarp();
@@ -376,6 +368,8 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
         t = s_next[it & 1];
     }
     if (P.stats && lane == 0 && surv_warp) atomicAdd(P.survivors_total, surv_warp);
+    oc.close(P.out, P.out_cap);
+    if (lane == 0 && oc.real) atomicAdd(P.match_total, (unsigned long long)oc.real);
     cand_lane = __reduce_add_sync(0xffffffffu, cand_lane);
     if (lane == 0 && cand_lane) atomicAdd(P.candidates, (unsigned long long)cand_lane);
 }
