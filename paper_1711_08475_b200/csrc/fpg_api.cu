@@ -1029,31 +1029,34 @@ void download(fpg_batch* B, fpg_result* out) {
         out->offsets[nq] = pos;
     }
     if (stats) {
-        out->stats = static_cast<uint64_t*>(std::calloc(FPG_NSTATS * std::max<uint64_t>(nq, 1), sizeof(uint64_t)));
+        out->stats = static_cast<uint64_t*>(std::malloc(FPG_NSTATS * sizeof(uint64_t) * std::max<uint64_t>(nq, 1)));
         if (!out->stats) throw std::bad_alloc();
         const fpg_dict* D = B->dict;
         const uint64_t N = D->n;
-        // prefix sums of bucket counts for compatible-range queries
+        // length-compatible words per query length (QueryStats bookkeeping,
+        // dictionary.hpp:89-101): N for Levenshtein without the prefilter
         const int L1 = fpg::kMaxLen + 1;
-        for (uint64_t q = 0; q < nq; ++q) {
-            const int lq = (int)B->qlen[q];
-            uint64_t surv = 0;
-            for (auto& s : B->sb) surv += s->h_qsurv.p[q];
-            uint64_t comp = 0;
-            const bool all = o.metric == FPG_LEVENSHTEIN && !o.length_prefilter;
-            if (all) {
-                comp = N;
-            } else {
+        const bool all = o.metric == FPG_LEVENSHTEIN && !o.length_prefilter;
+        std::vector<uint64_t> comp_of(B->qmax_len + 1, N);
+        if (!all)
+            for (int lq = 0; lq <= B->qmax_len; ++lq) {
                 const int lo = o.metric == FPG_HAMMING ? lq : std::max(0, lq - o.k);
                 const int hi = o.metric == FPG_HAMMING ? lq : std::min(L1 - 1, lq + o.k);
-                for (int L = lo; L <= hi; ++L) comp += D->len_count[L];
+                uint64_t c = 0;
+                for (int L = lo; L <= hi; ++L) c += D->len_count[L];
+                comp_of[lq] = c;
             }
+        const size_t G = B->sb.size();
+        for (uint64_t q = 0; q < nq; ++q) {
+            uint64_t surv = 0;
+            for (size_t g = 0; g < G; ++g) surv += B->sb[g]->h_qsurv.p[q];
+            const uint64_t comp = comp_of[B->qlen[q]];
             uint64_t* st = out->stats + FPG_NSTATS * q;
+            const uint64_t verified = o.use_filter ? surv : comp;
             st[FPG_STAT_COMPARED] = N;
             st[FPG_STAT_REJECTED_BY_LENGTH] = N - comp;
-            const uint64_t verified = o.use_filter ? surv : comp;
-            st[FPG_STAT_VERIFIED] = verified;
             st[FPG_STAT_REJECTED_BY_FINGERPRINT] = comp - verified;
+            st[FPG_STAT_VERIFIED] = verified;
             st[FPG_STAT_MATCHES] = out->offsets[q + 1] - out->offsets[q];
         }
     }
