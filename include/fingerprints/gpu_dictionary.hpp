@@ -92,7 +92,7 @@ public:
             offs[i + 1] = blob.size();
         }
         const fpg_query_options o{static_cast<int32_t>(opt.metric), opt.k, opt.use_filter ? 1 : 0,
-                                  opt.length_prefilter ? 1 : 0, per_query ? 1 : 0};
+                                  opt.length_prefilter ? 1 : 0, per_query ? 1 : 0, 0};
         fpg_result res{};
         detail::check(fpg_query_batch(dict_.get(), reinterpret_cast<const std::uint8_t*>(blob.data()), offs.data(),
                                       queries.size(), &o, &res));

@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define FPG_ABI_VERSION 1
+#define FPG_ABI_VERSION 2
 
 /* status codes */
 #define FPG_OK 0
@@ -66,6 +66,9 @@ typedef struct {
     int32_t use_filter;
     int32_t length_prefilter;
     int32_t want_stats;
+    int32_t exhaustive;        /* 1: no fingerprint pruning at all, every length-compatible
+                                  pair is byte-verified (the reference's naive path,
+                                  bench.hpp:133-134; for timing T_n).  Results are identical. */
 } fpg_query_options;
 
 /* Per-query QueryStats (dictionary.hpp:19-34), in this order. */

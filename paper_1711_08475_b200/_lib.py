@@ -38,6 +38,7 @@ class FpgQueryOptions(ctypes.Structure):
         ("use_filter", ctypes.c_int32),
         ("length_prefilter", ctypes.c_int32),
         ("want_stats", ctypes.c_int32),
+        ("exhaustive", ctypes.c_int32),
     ]
 
 
@@ -90,6 +91,7 @@ FPG_SIGNATURES = {
 }
 
 FPG_OK, FPG_EINVAL, FPG_EUNSUPPORTED, FPG_ECUDA, FPG_ENOMEM = 0, -1, -2, -3, -4
+FPG_ABI_VERSION = 2  # include/fpg.h
 
 _fpg = None
 _corpus = None
@@ -114,6 +116,9 @@ def load_fpg() -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        if lib.fpg_abi_version() != FPG_ABI_VERSION:
+            raise ImportError(f"{LIBFPG} has ABI {lib.fpg_abi_version()}, these bindings expect "
+                              f"{FPG_ABI_VERSION}: rebuild it (__graft_entry__.build())")
         _fpg = lib
     return _fpg
 

@@ -768,7 +768,8 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         SP.match_total = S.counters.p + 5;
         SP.k = o.k;
         SP.stats = (o.want_stats && o.use_filter) ? 1 : 0;
-        SP.use_fp = supports(D->scheme.variant, o.metric) ? 1 : 0;
+        SP.use_fp = supports(D->scheme.variant, o.metric) && !o.exhaustive ? 1 : 0;
+        SP.exhaustive = o.exhaustive ? 1 : 0;
     } else {
         P.q_fp = Q.cmp.p;
         P.q_bytes = Q.bytes.p;

@@ -92,6 +92,7 @@ struct SliceParams {
     int32_t k;
     int32_t stats;
     int32_t use_fp;             // scheme fields bound this metric (variant_supports, fingerprint.hpp:36-38)
+    int32_t exhaustive;         // verify every pair: no fingerprint / sig' pruning (naive-path timing)
 };
 
 __device__ __forceinline__ int stride_of_len(int len) { return len <= 16 ? 16 : (len + 15) & ~15; }
@@ -330,17 +331,20 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 }
             }
             if (verify) {
+                if (!P.exhaustive) {
 #pragma unroll
-                for (int g = 0; g < S; ++g)
+                    for (int g = 0; g < S; ++g)
 #pragma unroll
-                    for (int h = 0; h < NQ; ++h)
+                        for (int h = 0; h < NQ; ++h)
 #pragma unroll
-                        for (int r = 0; r < SLX; ++r) FPG_CNT(h, r, qxor(pl[r][NP + g], FPG_QS(h, NP + g), FPG_QM(h, NP + g)));
+                            for (int r = 0; r < SLX; ++r)
+                                FPG_CNT(h, r, qxor(pl[r][NP + g], FPG_QS(h, NP + g), FPG_QM(h, NP + g)));
+                }
 #pragma unroll
                 for (int h = 0; h < NQ; ++h)
 #pragma unroll
                     for (int r = 0; r < SLX; ++r) {
-                        const uint32_t cand = valid[r] & ~(P.k ? c2[h][r] : c0[h][r]);
+                        const uint32_t cand = P.exhaustive ? valid[r] : valid[r] & ~(P.k ? c2[h][r] : c0[h][r]);
                         if (cand) {
                             s_queue[qn * kSliceThreads + tid] = make_uint2((j + h) | ((uint32_t)r << 16), cand);
                             ++qn;

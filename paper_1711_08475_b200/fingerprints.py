@@ -138,6 +138,16 @@ def english_default_letters() -> str:
     return "etaoinshrdlcumwfgypbvkjxqz"
 
 
+# Standard English unigram frequencies (percent), a..z.
+_EN_PCT = (8.167, 1.492, 2.782, 4.253, 12.702, 2.228, 2.015, 6.094, 6.966, 0.153, 0.772, 4.025, 2.406,
+           6.749, 7.507, 1.929, 0.095, 5.987, 6.327, 9.056, 2.758, 0.978, 2.360, 0.150, 1.974, 0.074)
+
+
+def english_letter_frequencies() -> list[tuple[int, float]]:
+    """letter_model.hpp:147-157: (symbol, weight) pairs of English letters."""
+    return [(ord("a") + i, w) for i, w in enumerate(_EN_PCT)]
+
+
 # ---------------------------------------------------------------- schemes
 
 class Scheme:
@@ -297,12 +307,14 @@ class QueryOptions:
     k: int = 1
     use_filter: bool = True
     length_prefilter: bool = False
+    exhaustive: bool = False  # B200: byte-verify every pair, no pruning (naive-path timing)
 
     def c_struct(self, want_stats: bool) -> FpgQueryOptions:
         o = FpgQueryOptions()
         o.metric, o.k = int(self.metric), int(self.k)
         o.use_filter, o.length_prefilter = int(bool(self.use_filter)), int(bool(self.length_prefilter))
         o.want_stats = int(bool(want_stats))
+        o.exhaustive = int(bool(self.exhaustive))
         return o
 
 

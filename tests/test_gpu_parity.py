@@ -244,6 +244,10 @@ def test_staged_batch_reruns_across_options(oracle):
             b.run(QueryOptions(metric, k, True, pre), want_stats=True)
             csr, st = b.download()
             assert_same(csr, st, *oracle.query_batch(blob, offs, qblob, qoffs, osch(s), metric, k, True, pre))
+            # exhaustive (no pruning, every pair byte-verified): same matches, filter-off stats
+            b.run(QueryOptions(metric, k, False, pre, exhaustive=True), want_stats=True)
+            csr, st = b.download()
+            assert_same(csr, st, *oracle.query_batch(blob, offs, qblob, qoffs, osch(s), metric, k, False, pre))
 
 
 @pytest.mark.slow

@@ -32,7 +32,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), f"libfpg.so does not export {s}"
     assert set(syms) == set(FPG_SIGNATURES), "ctypes table out of sync with include/fpg.h"
-    assert lib.fpg_abi_version() == 1
+    assert lib.fpg_abi_version() == 2
 
 
 def test_library_is_sm100a_cuda():
