@@ -30,7 +30,7 @@ extern "C" {
 /* status codes */
 #define FPG_OK 0
 #define FPG_EINVAL -1        /* std::invalid_argument in the reference */
-#define FPG_EUNSUPPORTED -2  /* valid for the reference, not built for the GPU (e.g. k > 1) */
+#define FPG_EUNSUPPORTED -2  /* valid for the reference, not built for the GPU (k > 8) */
 #define FPG_ECUDA -3         /* CUDA runtime failure (no device, OOM, launch error) */
 #define FPG_ENOMEM -4        /* host allocation failure */
 
@@ -62,7 +62,7 @@ typedef struct {
  * QueryStats* argument being non-null, dictionary.hpp:66,75). */
 typedef struct {
     int32_t metric;
-    int32_t k;                 /* GPU path supports k in {0, 1} */
+    int32_t k;                 /* 0..8: k <= 1 bit-sliced K2, k >= 2 generic K2 + banded verifier */
     int32_t use_filter;
     int32_t length_prefilter;
     int32_t want_stats;

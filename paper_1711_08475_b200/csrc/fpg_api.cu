@@ -524,15 +524,15 @@ void launch_w(int width, bool stats, const fpg::Tile* tiles, uint32_t ntiles, co
 // Distance form per scheme: plain popcount (occurrence, halved, one-hot
 // count-16), compile-time folds for count b=2/4 and position p=3, else the
 // generic runtime fold.
-int dist_kind(const fpg::SchemeParams& S) {
-    if (S.variant == FPG_OCCURRENCE || S.variant == FPG_OCCURRENCE_HALVED || S.onehot) return fpg::kPopc;
+int dist_kind(const fpg::SchemeParams& S, bool onehot) {
+    if (S.variant == FPG_OCCURRENCE || S.variant == FPG_OCCURRENCE_HALVED || onehot) return fpg::kPopc;
     if (S.variant == FPG_COUNT) return S.b == 2 ? fpg::kFold2 : S.b == 4 ? fpg::kFold4 : fpg::kGeneric;
     return S.p == 3 ? fpg::kPos3 : fpg::kGeneric;
 }
 
-void dispatch_scan(const fpg::SchemeParams& S, bool stats, const fpg::Tile* tiles, uint32_t ntiles,
+void dispatch_scan(const fpg::SchemeParams& S, bool onehot, bool stats, const fpg::Tile* tiles, uint32_t ntiles,
                    const fpg::ScanParams& P, cudaStream_t st, int device) {
-    switch (dist_kind(S)) {
+    switch (dist_kind(S, onehot)) {
         case fpg::kPopc: launch_w<fpg::kPopc>(S.width, stats, tiles, ntiles, P, st, device); break;
         case fpg::kFold2: launch_w<fpg::kFold2>(S.width, stats, tiles, ntiles, P, st, device); break;
         case fpg::kFold4: launch_w<fpg::kFold4>(S.width, stats, tiles, ntiles, P, st, device); break;
@@ -633,10 +633,14 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
     // The tile plan depends only on the batch's length histogram and the
     // options: it is built (and uploaded) once and reused by later runs and
     // by later batches with the same histogram.
+    // the bit-sliced K2 covers k <= 1; larger k runs the generic per-pair
+    // kernel (POPC filter, banded verifier) on the same collections
+    const bool use_slice = D->slice && o.k <= 1;
+    const bool from_slice = D->slice && !use_slice;  // generic kernel over bit-sliced collections
     const bool replan = !S.plan_valid || std::memcmp(&S.plan_opts, &o, sizeof(o)) != 0;
     if (!replan) {
         executed = S.executed;
-    } else if (D->slice) {
+    } else if (use_slice) {
         splan.clear();
         // Tile plan: per word length lw, the compatible query lengths form one
         // contiguous range of the length-sorted queries (Hamming / k = 0:
@@ -747,7 +751,7 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
 
     fpg::ScanParams P{};
     fpg::SliceParams SP{};
-    if (D->slice) {
+    if (use_slice) {
         SP.planes = W.planes.p;
         SP.q_fp = Q.fp.p;
         SP.q_sigp = Q.sigp.p;
@@ -771,12 +775,17 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         SP.use_fp = supports(D->scheme.variant, o.metric) && !o.exhaustive ? 1 : 0;
         SP.exhaustive = o.exhaustive ? 1 : 0;
     } else {
-        P.q_fp = Q.cmp.p;
+        // comparison words: the reference-layout fingerprints when the
+        // collections were built for k_slice (no one-hot form, no signatures)
+        const bool onehot = D->params.onehot && !from_slice;
+        P.q_fp = from_slice ? Q.fp.p : Q.cmp.p;
+        P.w_fp = from_slice ? W.fp.p : W.cmp.p;
         P.q_bytes = Q.bytes.p;
         P.q_ids = Q.ids.p;
-        P.w_fp = W.cmp.p;
         P.q_sig = Q.sig.p;
         P.w_sig = W.sig.p;
+        P.sig_on = (!from_slice && o.k <= 1) ? 1 : 0;
+        P.lev = o.metric == FPG_LEVENSHTEIN ? 1 : 0;
         P.w_bytes = W.bytes.p;
         P.w_ids = W.ids.p;
         P.id_base = D->id_base + sh.base;
@@ -787,7 +796,7 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         P.mask_single = D->params.mask_single;
         // reject iff F_D > 2k (ceil_half(F_D) > k, dictionary.hpp:102-106); the
         // one-hot count form counts every differing field twice
-        P.thr = o.use_filter ? (D->params.onehot ? 4 * o.k : 2 * o.k) : 1 << 20;
+        P.thr = o.use_filter ? (onehot ? 4 * o.k : 2 * o.k) : 1 << 20;
         P.k = o.k;
         P.fold = D->params.variant == FPG_COUNT ? D->params.b
                : D->params.variant == FPG_POSITION ? D->params.p : 1;
@@ -809,11 +818,12 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
             if (nq) CK(cudaMemsetAsync(S.qsurv.p, 0, 2 * nq * sizeof(uint32_t), st));
         }
         CK(cudaEventRecord(S.ev[1], st));
-        if (D->slice && !splan.empty()) {
+        if (use_slice && !splan.empty()) {
             dispatch_slice(D->scheme, D->params.nsig, S.stiles.p, (uint32_t)splan.size(), SP, st, sh.device);
             ++S.launches;
-        } else if (!D->slice && !plan.empty()) {
-            dispatch_scan(D->params, o.want_stats != 0, S.tiles.p, (uint32_t)plan.size(), P, st, sh.device);
+        } else if (!use_slice && !plan.empty()) {
+            dispatch_scan(D->params, D->params.onehot && !from_slice, o.want_stats != 0, S.tiles.p,
+                          (uint32_t)plan.size(), P, st, sh.device);
             ++S.launches;
         }
         CK(cudaEventRecord(S.ev[2], st));
@@ -892,8 +902,10 @@ void check_opts(const fpg_dict* D, const fpg_query_options* o) {
     if (o->metric != FPG_HAMMING && o->metric != FPG_LEVENSHTEIN) throw Error(FPG_EINVAL, "unknown metric");
     if (o->use_filter && !supports(D->scheme.variant, o->metric))
         throw Error(FPG_EINVAL, "scheme does not filter for this metric");
-    if (o->k < 0 || o->k > 1)
-        throw Error(FPG_EUNSUPPORTED, "GPU scan supports k in {0, 1}, got " + std::to_string(o->k));
+    if (o->k < 0) throw Error(FPG_EINVAL, "k must be >= 0");
+    if (o->k > fpg::kMaxK)
+        throw Error(FPG_EUNSUPPORTED, "GPU scan supports k <= " + std::to_string(fpg::kMaxK) + ", got " +
+                                          std::to_string(o->k));
 }
 
 void upload(fpg_batch* B, const uint8_t* qbytes, const uint64_t* qoffsets, uint64_t nq) {

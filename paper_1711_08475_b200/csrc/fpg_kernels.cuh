@@ -66,6 +66,8 @@ struct ScanParams {
     int32_t fold;               // field width for the generic fold (kGeneric only)
     const uint32_t* q_sig;      // occurrence signatures (verifier pre-check)
     const uint32_t* w_sig;
+    int32_t sig_on;             // signature pre-check (exact for k <= 1 only)
+    int32_t lev;                // metric is Levenshtein (k >= 2 verifier)
     uint32_t* q_matches;        // per input query: matches (K4 segment sizes)
 };
 

@@ -139,6 +139,63 @@ __device__ __forceinline__ bool verify_regs(const uint32_t (&q)[NW], const uint3
     return lb < fa;
 }
 
+// k >= 2 verification from global memory (zero-padded strings).
+constexpr int kMaxK = 8;  // largest k the GPU scan accepts
+
+// hamming_bounded (edit_distance.hpp:18-27) as a test: equal lengths, at most
+// k mismatching bytes.  Padding is zero on both sides, so whole 4-byte words
+// compare; bytes that differ are counted per word.
+__device__ __forceinline__ bool hamming_le(const uint8_t* a, const uint8_t* b, int n, int k) {
+    int mism = 0;
+    for (int c = 0; c < n; c += 4) {
+        uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(a + c)) ^ __ldg(reinterpret_cast<const uint32_t*>(b + c));
+        x = (x | (x >> 4)) & 0x0f0f0f0fu;
+        x = (x | (x >> 2)) & 0x03030303u;
+        x = (x | (x >> 1)) & 0x01010101u;
+        mism += __popc(x);
+        if (mism > k) return false;
+    }
+    return true;
+}
+
+// levenshtein_bounded (edit_distance.hpp:31-64) as a test: the 2k+1-wide
+// band of the DP, cell (i, j) at band index t = j - i + k, early exit when a
+// row's minimum exceeds k.
+__device__ __noinline__ bool levenshtein_le(const uint8_t* s1, int m, const uint8_t* s2, int n, int k) {
+    if (m > n) {
+        const uint8_t* ts = s1; s1 = s2; s2 = ts;
+        const int tn = m; m = n; n = tn;
+    }
+    if (n - m > k) return false;
+    const int inf = k + 1, w = 2 * k + 1;
+    int prev[2 * kMaxK + 1], cur[2 * kMaxK + 1];
+    for (int t = 0; t < w; ++t) {  // row 0: D[0][j] = j
+        const int j = t - k;
+        prev[t] = (j < 0 || j > n || j > k) ? inf : j;
+    }
+    for (int i = 1; i <= m; ++i) {
+        const uint8_t a = __ldg(s1 + i - 1);
+        int best = inf;
+        for (int t = 0; t < w; ++t) {
+            const int j = i - k + t;
+            int v = inf;
+            if (j == 0) {
+                v = i < inf ? i : inf;
+            } else if (j > 0 && j <= n) {
+                v = prev[t] + (a != __ldg(s2 + j - 1));               // substitution / match
+                if (t + 1 < w) v = min(v, prev[t + 1] + 1);           // deletion
+                if (t > 0) v = min(v, cur[t - 1] + 1);                // insertion
+                v = min(v, inf);
+            }
+            cur[t] = v;
+            best = min(best, v);
+        }
+        if (best > k) return false;
+        for (int t = 0; t < w; ++t) prev[t] = cur[t];
+    }
+    return prev[n - m + k] <= k;
+}
+
 template <int NW>
 __device__ __forceinline__ void load_padded(const uint8_t* p, int stride, uint32_t (&r)[NW]) {
     const uint4 a = __ldg(reinterpret_cast<const uint4*>(p));
@@ -230,6 +287,8 @@ struct TileScan {
     __device__ __forceinline__ bool verify_bytes(uint32_t j, uint32_t widx) const {
         const uint8_t* qb = qbytes + (uint64_t)j * qs;
         const uint8_t* wb = wbytes + (uint64_t)widx * ws;
+        if (P.k >= 2) return m == n ? hamming_le(qb, wb, m, P.k) || (P.lev && levenshtein_le(qb, m, wb, n, P.k))
+                                    : P.lev && levenshtein_le(qb, m, wb, n, P.k);
         if (vclass == 1) {
             uint32_t a[4], b[4];
             load_padded<4>(qb, qs, a);
@@ -305,8 +364,8 @@ struct TileScan {
             const uint32_t j1 = two ? j + 1 : j;
             const T q0 = lds_t<T>(a_q + (uint32_t)sizeof(T) * j);
             const T q1 = lds_t<T>(a_q + (uint32_t)sizeof(T) * j1);
-            const uint32_t g0 = lds32(a_qsig + 4u * j);
-            const uint32_t g1 = lds32(a_qsig + 4u * j1);
+            const uint32_t g0 = P.sig_on ? lds32(a_qsig + 4u * j) : 0u;
+            const uint32_t g1 = P.sig_on ? lds32(a_qsig + 4u * j1) : 0u;
             uint32_t d[2][kWordsPerLane], s[2][kWordsPerLane];
 #pragma unroll
             for (int r = 0; r < kWordsPerLane; ++r) {
@@ -372,7 +431,7 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(const Tile* __restrict
         __syncthreads();  // previous tile's shared state fully consumed
         for (uint32_t i = tid; i < tl.q_count; i += kScanThreads) {
             s_q[i] = (T)P.q_fp[tl.q_begin + i];
-            s_qsig[i] = P.q_sig[tl.q_begin + i];
+            s_qsig[i] = P.sig_on ? P.q_sig[tl.q_begin + i] : 0u;
         }
         T wc[kWordsPerLane];
         uint32_t wg[kWordsPerLane];
@@ -382,7 +441,7 @@ __global__ void __launch_bounds__(kScanThreads, 4) k_scan(const Tile* __restrict
             const uint32_t widx = r * kScanThreads + tid;
             const bool ok = widx < tl.w_count;
             wc[r] = ok ? (T)P.w_fp[tl.w_begin + widx] : (T)0;
-            wg[r] = ok ? P.w_sig[tl.w_begin + widx] : 0u;
+            wg[r] = ok && P.sig_on ? P.w_sig[tl.w_begin + widx] : 0u;
             // flag bits of word r = 4h + t for both queries: bit 8t + 7 - k, k = 2 qi + h
             if (ok) vmask |= (1u << (8 * (r & 3) + 7 - (r >> 2))) | (1u << (8 * (r & 3) + 5 - (r >> 2)));
         }

@@ -113,7 +113,7 @@ def main() -> None:
     for s in SCHEMES[:4]:
         d = ref.dictionary(dblob, doffs, s["variant"], s["letters"], s["b"], s["p"])
         for metric in (0, 1):
-            for k in (0, 1):
+            for k in (0, 1, 2, 3):
                 for use_filter in (True, False):
                     for pre in (False, True):
                         if use_filter and not (metric == 0 or s["variant"] in (0, 2)):

@@ -8,7 +8,7 @@ import pytest
 
 from oracle.oracle import oscheme, pack
 from paper_1711_08475_b200 import (GpuFingerprintedDictionary, LetterSet, Metric, QueryOptions,
-                                   QueryStats, Scheme, Variant, build, build_many, render)
+                                   QueryStats, Scheme, Variant, build, build_many, render, variant_supports)
 from paper_1711_08475_b200.corpus import (CELLS, generate_dictionary, generate_queries, make_scheme,
                                           subsample)
 
@@ -150,8 +150,9 @@ def test_config_cells_vs_oracle(oracle, cfg, n, nq):
 
 
 @pytest.mark.parametrize("metric", [Metric.Hamming, Metric.Levenshtein])
-@pytest.mark.parametrize("k", [0, 1])
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
 def test_filter_off_and_k0(oracle, metric, k):
+    """k = 0..3 (k >= 2 runs the generic kernel and the banded verifier), filter on/off."""
     blob, offs, qblob, qoffs = _cfg_inputs(2, 50_000, 300)
     s = make_scheme(blob, Variant.Count, 16)
     with GpuFingerprintedDictionary((blob, offs), s) as d:
@@ -184,6 +185,20 @@ def test_edge_strings(oracle):
                 assert_same(csr, st, *oracle.query_batch(blob, offs, qblob, qoffs, osch(s), metric, 1, True, pre))
 
 
+@pytest.mark.parametrize("variant,width", [(Variant.Occurrence, 16), (Variant.Count, 32), (Variant.Position, 64)])
+def test_k_above_one_other_schemes(oracle, variant, width):
+    """k = 2 on bit-sliced dictionaries of other widths, Hamming and (where the
+    scheme filters it) Levenshtein, without and with the length prefilter."""
+    blob, offs, qblob, qoffs = _cfg_inputs(5, 40_000, 200)
+    s = make_scheme(blob, variant, width)
+    with GpuFingerprintedDictionary((blob, offs), s) as d:
+        for metric in (Metric.Hamming, Metric.Levenshtein):
+            use_filter = variant_supports(variant, metric)
+            for pre in (True, False):
+                csr, st = d.query_batch((qblob, qoffs), QueryOptions(metric, 2, use_filter, pre), per_query_stats=True)
+                assert_same(csr, st, *oracle.query_batch(blob, offs, qblob, qoffs, osch(s), metric, 2, use_filter, pre))
+
+
 def test_too_long_and_invalid_args():
     s = Scheme.occurrence(LetterSet("etaoinshrdlcumwf"))
     with pytest.raises(ValueError):
@@ -193,8 +208,11 @@ def test_too_long_and_invalid_args():
     with pytest.raises(ValueError):
         Scheme.count(LetterSet("etaoinsh"), 3)
     with GpuFingerprintedDictionary(["abc"], s) as d:
+        assert d.query("abd", QueryOptions(Metric.Hamming, 2)) == [0]  # k >= 2: generic kernel
         with pytest.raises(Exception):
-            d.query("abc", QueryOptions(Metric.Hamming, 2))  # k > 1 not built for the GPU
+            d.query("abc", QueryOptions(Metric.Hamming, 9))  # k > kMaxK is not built for the GPU
+        with pytest.raises(ValueError):
+            d.query("abc", QueryOptions(Metric.Hamming, -1))
         csr, st = d.query_batch([], QueryOptions(), per_query_stats=True)
         assert len(csr) == 0 and st.shape == (0, 5)
 
