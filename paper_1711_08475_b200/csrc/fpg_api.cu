@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -184,7 +185,7 @@ bool supports(int variant, int metric) {
     return metric == FPG_HAMMING || variant == FPG_OCCURRENCE || variant == FPG_COUNT;
 }
 
-uint64_t g_launches = 0;
+std::atomic<uint64_t> g_launches{0};  // per process; per-run counts are exact
 
 const bool g_trace = [] {
     const char* e = std::getenv("FPG_TRACE");

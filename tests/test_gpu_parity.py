@@ -199,6 +199,31 @@ def test_k_above_one_other_schemes(oracle, variant, width):
                 assert_same(csr, st, *oracle.query_batch(blob, offs, qblob, qoffs, osch(s), metric, 2, use_filter, pre))
 
 
+def test_concurrent_query_batches(oracle):
+    """Concurrent const queries are safe in the reference (README.md:124-125):
+    four host threads share one dictionary handle, each with its own batch."""
+    import threading
+
+    blob, offs, qblob, qoffs = _cfg_inputs(2, 80_000, 300)
+    s = make_scheme(blob, Variant.Count, 16)
+    want = oracle.query_batch(blob, offs, qblob, qoffs, osch(s), Metric.Levenshtein, 1, True, True)
+    errors = []
+    with GpuFingerprintedDictionary((blob, offs), s) as d:
+        def worker():
+            try:
+                for _ in range(5):
+                    csr, st = d.query_batch((qblob, qoffs), QueryOptions(Metric.Levenshtein, 1, True, True), True)
+                    assert_same(csr, st, *want)
+            except Exception as e:  # reported below
+                errors.append(e)
+        th = [threading.Thread(target=worker) for _ in range(4)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+    assert not errors, errors[0]
+
+
 def test_too_long_and_invalid_args():
     s = Scheme.occurrence(LetterSet("etaoinshrdlcumwf"))
     with pytest.raises(ValueError):
