@@ -56,7 +56,7 @@ class GpuFingerprintedDictionary {
 public:
     GpuFingerprintedDictionary(std::vector<std::string> words, Scheme scheme, std::vector<int> devices = {0},
                                std::uint64_t id_base = 0)
-        : words_(std::move(words)), scheme_(std::move(scheme)) {
+        : words_(std::move(words)), scheme_(std::move(scheme)), n_(words_.size()) {
         std::vector<std::uint64_t> offs(words_.size() + 1, 0);
         std::string blob;
         for (std::size_t i = 0; i < words_.size(); ++i) {
@@ -71,11 +71,28 @@ public:
         dict_.reset(d);
     }
 
+    // Newline-separated word text (read_word_lines, corpus.hpp:116-125) split
+    // into words on the GPU(s); words() stays empty.
+    static GpuFingerprintedDictionary from_text(std::string_view text, Scheme scheme, std::vector<int> devices = {0},
+                                                std::uint64_t id_base = 0) {
+        GpuFingerprintedDictionary d(std::move(scheme));
+        std::vector<int32_t> devs(devices.begin(), devices.end());
+        const fpg_scheme s = d.scheme_.c_struct();
+        fpg_dict* h = nullptr;
+        detail::check(fpg_dict_create_from_text(reinterpret_cast<const std::uint8_t*>(text.data()), text.size(), &s,
+                                                devs.data(), static_cast<int32_t>(devs.size()), id_base, &h));
+        d.dict_.reset(h);
+        std::uint64_t n = 0;
+        detail::check(fpg_dict_size(h, &n));
+        d.n_ = n;
+        return d;
+    }
+
     [[nodiscard]] const std::vector<std::string>& words() const { return words_; }
     [[nodiscard]] const Scheme& scheme() const { return scheme_; }
-    [[nodiscard]] std::size_t size() const { return words_.size(); }
+    [[nodiscard]] std::size_t size() const { return n_; }
     [[nodiscard]] std::vector<Fingerprint> prints() const {
-        std::vector<std::uint64_t> raw(words_.size());
+        std::vector<std::uint64_t> raw(n_);
         detail::check(fpg_dict_prints(dict_.get(), raw.data()));
         std::vector<Fingerprint> out(raw.size());
         for (std::size_t i = 0; i < raw.size(); ++i) out[i].bits = raw[i];
@@ -129,11 +146,13 @@ public:
     }
 
 private:
+    explicit GpuFingerprintedDictionary(Scheme scheme) : scheme_(std::move(scheme)) {}
     struct Deleter {
         void operator()(fpg_dict* d) const { fpg_dict_destroy(d); }
     };
     std::vector<std::string> words_;
     Scheme scheme_;
+    std::uint64_t n_ = 0;
     std::unique_ptr<fpg_dict, Deleter> dict_;
 };
 

@@ -44,6 +44,9 @@ inline SymbolFrequencyTable compute_frequencies(const std::vector<std::string>& 
     return t;
 }
 
+// compute_frequencies of a large blob on the GPU (libfpg.so).
+inline SymbolFrequencyTable compute_frequencies_gpu(std::string_view text, int device = 0);
+
 enum class LetterStrategy { Common, Mixed, Rare };
 
 inline std::string_view to_string(LetterStrategy s) {

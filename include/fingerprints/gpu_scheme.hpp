@@ -143,6 +143,15 @@ private:
     int width_;
 };
 
+inline SymbolFrequencyTable compute_frequencies_gpu(std::string_view text, int device) {
+    SymbolFrequencyTable t;
+    std::uint64_t counts[256] = {0};
+    detail::check(fpg_byte_histogram(reinterpret_cast<const std::uint8_t*>(text.data()), text.size(), device, counts));
+    for (int c = 0; c < 256; ++c) t.counts[static_cast<std::size_t>(c)] = counts[c];
+    t.total = text.size();
+    return t;
+}
+
 // build() for a batch of strings, on `device` (K1).
 inline std::vector<Fingerprint> build_many(const std::vector<std::string>& words, const Scheme& scheme,
                                            int device = 0) {

@@ -112,6 +112,12 @@ int fpg_scheme_supports(const fpg_scheme* scheme, int32_t metric);
 int fpg_dict_create(const uint8_t* bytes, const uint64_t* offsets, uint64_t n,
                     const fpg_scheme* scheme, const int32_t* devices, int32_t ndevices,
                     uint64_t id_base, fpg_dict** out);
+/* The same dictionary from a newline-separated word text (read_word_lines,
+ * corpus.hpp:116-125: one word per line, a trailing newline does not add an
+ * empty word, bytes are kept raw).  The text is split on the GPU(s): newline
+ * positions, newline-free bytes and word offsets never exist on the host. */
+int fpg_dict_create_from_text(const uint8_t* text, uint64_t nbytes, const fpg_scheme* scheme,
+                              const int32_t* devices, int32_t ndevices, uint64_t id_base, fpg_dict** out);
 int fpg_dict_destroy(fpg_dict* dict);
 /* FingerprintedDictionary::size() (dictionary.hpp:62) */
 int fpg_dict_size(const fpg_dict* dict, uint64_t* n);
@@ -120,6 +126,10 @@ int fpg_dict_size(const fpg_dict* dict, uint64_t* n);
 int fpg_dict_prints(const fpg_dict* dict, uint64_t* out);
 /* Seconds the construction took (upload + K1 + layout), like bench.hpp:118-120. */
 int fpg_dict_build_seconds(const fpg_dict* dict, double* seconds);
+
+/* compute_frequencies (letter_model.hpp:33-45) on `device`: counts[256] of
+ * the bytes (for select_letters over large corpora). */
+int fpg_byte_histogram(const uint8_t* bytes, uint64_t nbytes, int32_t device, uint64_t* counts);
 
 /* build() (fingerprint.hpp:276-284) for n strings on one device. */
 int fpg_build_fingerprints(const uint8_t* bytes, const uint64_t* offsets, uint64_t n,

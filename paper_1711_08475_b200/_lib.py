@@ -64,6 +64,10 @@ FPG_SIGNATURES = {
                                        ctypes.POINTER(FpgScheme), ctypes.POINTER(ctypes.c_int32),
                                        ctypes.c_int32, ctypes.c_uint64,
                                        ctypes.POINTER(ctypes.c_void_p)]),
+    "fpg_dict_create_from_text": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(FpgScheme),
+                                                 ctypes.POINTER(ctypes.c_int32), ctypes.c_int32, ctypes.c_uint64,
+                                                 ctypes.POINTER(ctypes.c_void_p)]),
+    "fpg_byte_histogram": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int32, ctypes.c_void_p]),
     "fpg_dict_destroy": (ctypes.c_int, [ctypes.c_void_p]),
     "fpg_dict_size": (ctypes.c_int, [ctypes.c_void_p, c_u64p]),
     "fpg_dict_prints": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),

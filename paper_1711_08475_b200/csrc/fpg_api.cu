@@ -26,6 +26,8 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include "../../include/fpg.h"
 #include "fpg_kernels.cuh"
@@ -1143,6 +1145,96 @@ int fpg_scheme_supports(const fpg_scheme* scheme, int32_t metric) {
     return scheme && supports(scheme->variant, metric) ? 1 : 0;
 }
 
+namespace {
+
+std::vector<int32_t> checked_devices(const int32_t* devices, int32_t ndevices) {
+    std::vector<int32_t> devs;
+    if (devices && ndevices > 0) devs.assign(devices, devices + ndevices);
+    else devs.push_back(0);
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    for (int d : devs)
+        if (d < 0 || d >= ndev) throw Error(FPG_EINVAL, "device " + std::to_string(d) + " not present");
+    return devs;
+}
+
+std::unique_ptr<fpg_dict> new_dict(const fpg_scheme* scheme, uint64_t id_base, const std::vector<int32_t>& devs) {
+    auto D = std::make_unique<fpg_dict>();
+    D->scheme = *scheme;
+    D->params = make_params(*scheme);
+    D->id_base = id_base;
+    D->len_count.assign(fpg::kMaxLen + 1, 0);
+    for (int32_t d : devs) {
+        auto sh = std::make_unique<Shard>();
+        sh->device = d;
+        D->shards.push_back(std::move(sh));
+    }
+    return D;
+}
+
+// Contiguous input-order id ranges, one per shard.
+void assign_ranges(fpg_dict& D, uint64_t n) {
+    if (n >= (1ull << 32) - 1) throw Error(FPG_EINVAL, "dictionary too large for 32-bit ids");
+    if (D.id_base + n > (1ull << 32)) throw Error(FPG_EINVAL, "id_base + n exceeds 32-bit ids");
+    D.n = n;
+    const size_t G = D.shards.size();
+    for (size_t g = 0; g < G; ++g) {
+        D.shards[g]->base = n * g / G;
+        D.shards[g]->n = n * (g + 1) / G - D.shards[g]->base;
+    }
+}
+
+void byte_histogram(const uint8_t* d_bytes, uint64_t nbytes, unsigned long long* d_hist, cudaStream_t st) {
+    CK(cudaMemsetAsync(d_hist, 0, 256 * sizeof(unsigned long long), st));
+    if (nbytes) {
+        fpg::k_hist256<<<(unsigned)std::min<uint64_t>(cdiv(nbytes, 256), 4096), 256, 0, st>>>(d_bytes, nbytes, d_hist);
+        CK(cudaGetLastError());
+    }
+}
+
+// Phase 2 of construction, after every shard's strings are on its device
+// (sh.blob, sh.offs + offs_at[g]) and `hist` counts the dictionary's bytes:
+// the K2 path and sig' map, then fingerprints, length buckets, padded bytes
+// and planes per shard.
+void finish_dict(fpg_dict& D, const std::vector<unsigned long long>& hist, const std::vector<uint64_t>& offs_at,
+                 std::chrono::steady_clock::time_point t0) {
+    configure_slice(D, hist);
+    for_each_shard(D.shards.size(), [&](size_t g) {
+        Shard& sh = *D.shards[g];
+        CK(cudaSetDevice(sh.device));
+        sh.dict.build(sh.blob.p, sh.offs.p + offs_at[g], sh.n, D.params, sh.stream,
+                      D.slice ? kSliceDict : kGenericDict, D.npt);
+        CK(cudaStreamSynchronize(sh.stream));
+        sh.dict.drop_scratch();
+        sh.blob.release();
+        sh.offs.release();
+    });
+    for (auto& sh : D.shards)
+        for (int L = 0; L <= fpg::kMaxLen; ++L) D.len_count[L] += sh->dict.count[L];
+    D.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+struct IsNewline {
+    const uint8_t* t;
+    __device__ bool operator()(uint64_t i) const { return t[i] == '\n'; }
+};
+struct NotNewline {
+    __device__ bool operator()(uint8_t c) const { return c != '\n'; }
+};
+
+// Word i of a newline-separated text, after the newlines are removed
+// (read_word_lines, corpus.hpp:116-125: a trailing newline ends the last word,
+// empty lines are empty words): offsets[i] = nl[i-1] + 1 - i, offsets[n] =
+// bytes left.
+__global__ void k_text_offsets(const uint64_t* __restrict__ nl, uint64_t n, uint64_t kept,
+                               uint64_t* __restrict__ offsets) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    offsets[i] = i == 0 ? 0 : i == n ? kept : nl[i - 1] + 1 - i;
+}
+
+}  // namespace
+
 int fpg_dict_create(const uint8_t* bytes, const uint64_t* offsets, uint64_t n, const fpg_scheme* scheme,
                     const int32_t* devices, int32_t ndevices, uint64_t id_base, fpg_dict** out) {
     return guarded([&] {
@@ -1150,30 +1242,11 @@ int fpg_dict_create(const uint8_t* bytes, const uint64_t* offsets, uint64_t n, c
         if (!out) throw Error(FPG_EINVAL, "null output handle");
         if (n && !offsets) throw Error(FPG_EINVAL, "null dictionary offsets");
         if (n && offsets[n] > offsets[0] && !bytes) throw Error(FPG_EINVAL, "null dictionary bytes");
-        if (n >= (1ull << 32) - 1) throw Error(FPG_EINVAL, "dictionary too large for 32-bit ids");
-        if (id_base + n > (1ull << 32)) throw Error(FPG_EINVAL, "id_base + n exceeds 32-bit ids");
-        std::vector<int32_t> devs;
-        if (devices && ndevices > 0) devs.assign(devices, devices + ndevices);
-        else devs.push_back(0);
-        int ndev = 0;
-        CK(cudaGetDeviceCount(&ndev));
-        for (int d : devs)
-            if (d < 0 || d >= ndev) throw Error(FPG_EINVAL, "device " + std::to_string(d) + " not present");
+        const std::vector<int32_t> devs = checked_devices(devices, ndevices);
         auto t0 = std::chrono::steady_clock::now();
-        auto D = std::make_unique<fpg_dict>();
-        D->scheme = *scheme;
-        D->params = make_params(*scheme);
-        D->n = n;
-        D->id_base = id_base;
-        D->len_count.assign(fpg::kMaxLen + 1, 0);
+        auto D = new_dict(scheme, id_base, devs);
+        assign_ranges(*D, n);
         const size_t G = devs.size();
-        for (size_t g = 0; g < G; ++g) {
-            auto sh = std::make_unique<Shard>();
-            sh->device = devs[g];
-            sh->base = n * g / G;
-            sh->n = n * (g + 1) / G - sh->base;
-            D->shards.push_back(std::move(sh));
-        }
         // Phase 1: upload each shard's strings and count its bytes (sig' ranking).
         for_each_shard(G, [&](size_t g) {
             Shard& sh = *D->shards[g];
@@ -1189,12 +1262,7 @@ int fpg_dict_create(const uint8_t* bytes, const uint64_t* offsets, uint64_t n, c
             CK(cudaMemcpyAsync(sh.offs.p, local.data(), (sh.n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, sh.stream));
             sh.d_hist.reserve(256);
             sh.h_hist.reserve(256);
-            CK(cudaMemsetAsync(sh.d_hist.p, 0, 256 * sizeof(unsigned long long), sh.stream));
-            if (nbytes) {
-                fpg::k_hist256<<<(unsigned)std::min<uint64_t>(cdiv(nbytes, 256), 4096), 256, 0, sh.stream>>>(
-                    sh.blob.p, nbytes, sh.d_hist.p);
-                CK(cudaGetLastError());
-            }
+            byte_histogram(sh.blob.p, nbytes, sh.d_hist.p, sh.stream);
             CK(cudaMemcpyAsync(sh.h_hist.p, sh.d_hist.p, 256 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                sh.stream));
             CK(cudaStreamSynchronize(sh.stream));
@@ -1202,22 +1270,88 @@ int fpg_dict_create(const uint8_t* bytes, const uint64_t* offsets, uint64_t n, c
         std::vector<unsigned long long> hist(256, 0);
         for (auto& sh : D->shards)
             for (int c = 0; c < 256; ++c) hist[c] += sh->h_hist.p[c];
-        configure_slice(*D, hist);
-        // Phase 2: fingerprints, length buckets, padded bytes and (bit-sliced) planes.
+        finish_dict(*D, hist, std::vector<uint64_t>(G, 0), t0);
+        *out = D.release();
+    });
+}
+
+int fpg_dict_create_from_text(const uint8_t* text, uint64_t nbytes, const fpg_scheme* scheme,
+                              const int32_t* devices, int32_t ndevices, uint64_t id_base, fpg_dict** out) {
+    return guarded([&] {
+        validate(scheme);
+        if (!out) throw Error(FPG_EINVAL, "null output handle");
+        if (nbytes && !text) throw Error(FPG_EINVAL, "null text");
+        const std::vector<int32_t> devs = checked_devices(devices, ndevices);
+        auto t0 = std::chrono::steady_clock::now();
+        auto D = new_dict(scheme, id_base, devs);
+        const size_t G = devs.size();
+        // Every device splits the whole text (HBM-bound, in parallel): newline
+        // positions, newline-free bytes and word offsets; each keeps its range.
+        std::vector<uint64_t> nwords(G, 0);
         for_each_shard(G, [&](size_t g) {
             Shard& sh = *D->shards[g];
             CK(cudaSetDevice(sh.device));
-            sh.dict.build(sh.blob.p, sh.offs.p, sh.n, D->params, sh.stream, D->slice ? kSliceDict : kGenericDict,
-                          D->npt);
-            CK(cudaStreamSynchronize(sh.stream));
-            sh.dict.drop_scratch();
-            sh.blob.release();
-            sh.offs.release();
+            CK(cudaStreamCreateWithFlags(&sh.stream, cudaStreamNonBlocking));
+            cudaStream_t st = sh.stream;
+            DBuf<uint8_t> dtext;
+            dtext.reserve(nbytes + 16);
+            if (nbytes) CK(cudaMemcpyAsync(dtext.p, text, nbytes, cudaMemcpyHostToDevice, st));
+            sh.d_hist.reserve(256);
+            sh.h_hist.reserve(256);
+            byte_histogram(dtext.p, nbytes, sh.d_hist.p, st);
+            CK(cudaMemcpyAsync(sh.h_hist.p, sh.d_hist.p, 256 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            const uint64_t nl = sh.h_hist.p[(unsigned char)'\n'];
+            const uint64_t kept = nbytes - nl;
+            const uint64_t n = nl + ((nbytes && text[nbytes - 1] != '\n') ? 1 : 0);
+            DBuf<uint64_t> pos;
+            DBuf<uint64_t> count;
+            DBuf<uint8_t> tmp;
+            pos.reserve(std::max<uint64_t>(nl, 1));
+            count.reserve(1);
+            sh.blob.reserve(kept + 16);
+            sh.offs.reserve(n + 1);
+            size_t tb = 0, tb2 = 0;
+            thrust::counting_iterator<uint64_t> idx(0);
+            CK(cub::DeviceSelect::If(nullptr, tb, idx, pos.p, count.p, (int64_t)nbytes, IsNewline{dtext.p}, st));
+            CK(cub::DeviceSelect::If(nullptr, tb2, dtext.p, sh.blob.p, count.p, (int64_t)nbytes, NotNewline{}, st));
+            tmp.reserve(std::max(tb, tb2));
+            if (nbytes) {
+                CK(cub::DeviceSelect::If(tmp.p, tb, idx, pos.p, count.p, (int64_t)nbytes, IsNewline{dtext.p}, st));
+                CK(cub::DeviceSelect::If(tmp.p, tb2, dtext.p, sh.blob.p, count.p, (int64_t)nbytes, NotNewline{}, st));
+            }
+            k_text_offsets<<<(unsigned)cdiv(n + 1, 256), 256, 0, st>>>(pos.p, n, kept, sh.offs.p);
+            CK(cudaGetLastError());
+            CK(cudaStreamSynchronize(st));
+            nwords[g] = n;
+            // histogram of the words themselves (the newlines are separators)
+            sh.h_hist.p[(unsigned char)'\n'] = 0;
         });
-        for (auto& sh : D->shards)
-            for (int L = 0; L <= fpg::kMaxLen; ++L) D->len_count[L] += sh->dict.count[L];
-        D->build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        assign_ranges(*D, nwords[0]);
+        std::vector<unsigned long long> hist(256, 0);
+        for (int c = 0; c < 256; ++c) hist[c] = D->shards[0]->h_hist.p[c];
+        std::vector<uint64_t> offs_at(G);
+        for (size_t g = 0; g < G; ++g) offs_at[g] = D->shards[g]->base;
+        finish_dict(*D, hist, offs_at, t0);
         *out = D.release();
+    });
+}
+
+int fpg_byte_histogram(const uint8_t* bytes, uint64_t nbytes, int32_t device, uint64_t* counts) {
+    return guarded([&] {
+        if (!counts || (nbytes && !bytes)) throw Error(FPG_EINVAL, "null argument");
+        CK(cudaSetDevice(device));
+        cudaStream_t st;
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        std::unique_ptr<CUstream_st, void (*)(CUstream_st*)> guard(st, [](CUstream_st* s) { cudaStreamDestroy(s); });
+        DBuf<uint8_t> d;
+        DBuf<unsigned long long> h;
+        d.reserve(nbytes);
+        h.reserve(256);
+        if (nbytes) CK(cudaMemcpyAsync(d.p, bytes, nbytes, cudaMemcpyHostToDevice, st));
+        byte_histogram(d.p, nbytes, h.p, st);
+        CK(cudaMemcpyAsync(counts, h.p, 256 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
     });
 }
 

@@ -80,6 +80,17 @@ class SymbolFrequencyTable:
         self.total += int(data.size)
 
 
+def compute_frequencies_gpu(data, device: int = 0) -> SymbolFrequencyTable:
+    """compute_frequencies over a large byte blob on the GPU (fpg_byte_histogram)."""
+    arr = data if isinstance(data, np.ndarray) else np.frombuffer(_as_bytes(data), np.uint8)
+    counts = np.zeros(256, np.uint64)
+    check(load_fpg().fpg_byte_histogram(ptr(arr), arr.size, device, ptr(counts)))
+    t = SymbolFrequencyTable()
+    t.counts = counts
+    t.total = int(arr.size)
+    return t
+
+
 def compute_frequencies(words) -> SymbolFrequencyTable:
     """letter_model.hpp:33-45: counts over the concatenated words (or a blob)."""
     t = SymbolFrequencyTable()
@@ -394,6 +405,31 @@ class GpuFingerprintedDictionary:
                                         len(devices), id_base, ctypes.byref(h)))
         self._h = h
         self._batch = None
+
+    @classmethod
+    def from_text(cls, text, scheme: Scheme, devices: Sequence[int] = (0,), id_base: int = 0):
+        """The dictionary of a newline-separated word text (read_word_lines,
+        corpus.hpp:116-125), split into words on the GPU(s).  ``text`` is
+        bytes, a uint8 array or a path; words() is not kept."""
+        if isinstance(text, (str,)) or hasattr(text, "__fspath__"):
+            with open(text, "rb") as f:
+                text = f.read()
+        data = text if isinstance(text, np.ndarray) else np.frombuffer(bytes(text), np.uint8)
+        self = cls.__new__(cls)
+        self._lib = load_fpg()
+        self._scheme = scheme
+        self._blob = self._offsets = None
+        devs = (ctypes.c_int32 * len(devices))(*devices)
+        sch = scheme.c_struct()
+        h = ctypes.c_void_p()
+        check(self._lib.fpg_dict_create_from_text(ptr(data), data.size, ctypes.byref(sch), devs, len(devices),
+                                                  id_base, ctypes.byref(h)))
+        self._h = h
+        self._batch = None
+        n = ctypes.c_uint64()
+        check(self._lib.fpg_dict_size(h, ctypes.byref(n)))
+        self._n = n.value
+        return self
 
     def close(self) -> None:
         if getattr(self, "_batch", None):

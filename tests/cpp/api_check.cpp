@@ -116,6 +116,14 @@ static int gpu_checks() {
             CHECK(per[q].verified == st.verified && per[q].rejected_by_length == st.rejected_by_length);
         }
     }
+    // the same dictionary split from its newline text on the GPU
+    std::string text;
+    for (const auto& w : words) text += w + "\n";
+    const FingerprintedDictionary from_text = FingerprintedDictionary::from_text(text, scheme);
+    CHECK(from_text.size() == words.size());
+    CHECK(from_text.prints() == dict.prints());
+    const auto freq_gpu = compute_frequencies_gpu(text);
+    CHECK(freq_gpu.counts[static_cast<unsigned char>('\n')] == words.size());
     bool threw = false;
     try {
         const Scheme p = Scheme::position(select_letters(compute_frequencies(words), 6, LetterStrategy::Common));

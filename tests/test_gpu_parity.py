@@ -328,3 +328,38 @@ def test_cpp_drop_in_queries(tmp_path):
     out = subprocess.run([str(exe), "gpu"], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr + out.stdout
     assert "api_check gpu: ok" in out.stdout
+
+
+@pytest.mark.parametrize("text", [b"", b"\n", b"a", b"a\n", b"a\n\nbc\r\nd", b"\n\n\n", b"xy\nz"])
+def test_dictionary_from_text_edges(text):
+    """fpg_dict_create_from_text splits like read_word_lines (corpus.hpp:116-125)."""
+    words = text.split(b"\n")
+    if text.endswith(b"\n"):
+        words = words[:-1]
+    if text == b"":
+        words = []
+    s = Scheme.occurrence(LetterSet("etaoinshrdlcumwf"))
+    with GpuFingerprintedDictionary.from_text(text, s) as d:
+        assert d.size() == len(words)
+        if words:
+            with GpuFingerprintedDictionary(words, s) as ref:
+                assert np.array_equal(d.prints_array(), ref.prints_array())
+                for pat in (b"a", b"bc\r", b"", b"z"):
+                    for m in (Metric.Hamming, Metric.Levenshtein):
+                        assert d.query(pat, QueryOptions(m, 1)) == ref.query(pat, QueryOptions(m, 1))
+
+
+def test_dictionary_from_text_config(oracle):
+    """A config-2 dictionary built from its newline text on two shards equals
+    the oracle (ids, stats), and the GPU byte histogram equals the host's."""
+    from paper_1711_08475_b200 import compute_frequencies, compute_frequencies_gpu
+
+    blob, offs, qblob, qoffs = _cfg_inputs(2, 120_000, 300)
+    words = [bytes(blob[int(offs[i]):int(offs[i + 1])]) for i in range(len(offs) - 1)]
+    text = b"\n".join(words) + b"\n"
+    s = make_scheme(blob, Variant.Count, 16)
+    assert np.array_equal(compute_frequencies_gpu(blob).counts, compute_frequencies(blob).counts)
+    with GpuFingerprintedDictionary.from_text(text, s, devices=(0, 0)) as d:
+        assert d.size() == len(words)
+        csr, st = d.query_batch((qblob, qoffs), QueryOptions(Metric.Levenshtein, 1, True, True), True)
+    assert_same(csr, st, *oracle.query_batch(blob, offs, qblob, qoffs, osch(s), Metric.Levenshtein, 1, True, True))
