@@ -331,6 +331,7 @@ def main():
     barrier()
     e2e_s = reduce_max(e2e_s, world)
     e2e_value = logical_pairs_all * args.steps / e2e_s
+
     assert np.array_equal(e2e_csr.word_ids, csr.word_ids), "e2e and staged results differ"
     h2d = int(qblob.nbytes + qoffs.nbytes)
     d2h = int(8 * (nq + 1) + 4 * int(csr.offsets[-1]) + 4 * nq)
@@ -370,7 +371,8 @@ def main():
         "matches_per_step": int(csr.offsets[-1]),
         "construction_s": build_s,
         "gpu_launches": launches,
-        "e2e": {"value": e2e_value, "unit": "comparisons/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": {"value": e2e_value, "unit": "comparisons/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "l2": "flushed between steps"},
         "roofline": {"bound": bound, "kernel": "k_slice (K2 filter+verify)" if shape["sliced"] else "k_scan (K2)",
                      "achieved": achieved, "peak": peak, "unit": "Tcmp/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",

@@ -400,8 +400,8 @@ struct fpg_dict {
     std::vector<std::unique_ptr<Shard>> shards;
     std::vector<uint64_t> len_count;  // whole-dictionary bucket counts (all shards)
     double build_seconds = 0;
-    std::mutex cache_mu;              // guards `cached` (fpg_query_batch reuses its scratch)
-    fpg_batch* cached = nullptr;
+    std::mutex cache_mu;              // guards `pool`
+    std::vector<fpg_batch*> pool;     // idle scratch batches of fpg_query_batch (one per concurrent caller)
     ~fpg_dict();
 };
 
@@ -409,6 +409,7 @@ namespace {
 
 struct ShardBatch {
     Shard* sh = nullptr;
+    cudaStream_t stream = nullptr;  // per batch: concurrent batches of one dictionary overlap
     DBuf<uint8_t> qblob;
     DBuf<uint64_t> qoffs;
     DBuf<uint32_t> qorder;
@@ -458,12 +459,13 @@ struct fpg_batch {
             cudaSetDevice(s->sh->device);
             for (auto e : s->ev)
                 if (e) cudaEventDestroy(e);
+            if (s->stream) cudaStreamDestroy(s->stream);
         }
     }
 };
 
 fpg_dict::~fpg_dict() {
-    delete cached;
+    for (fpg_batch* b : pool) delete b;
     for (auto& s : shards) {
         cudaSetDevice(s->device);
         if (s->stream) cudaStreamDestroy(s->stream);
@@ -614,7 +616,7 @@ bool compatible(int metric, int k, int lq, int lw) {
 void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options& o) {
     Shard& sh = *S.sh;
     CK(cudaSetDevice(sh.device));
-    cudaStream_t st = sh.stream;
+    cudaStream_t st = S.stream;
     for (auto& e : S.ev)
         if (!e) CK(cudaEventCreate(&e));
     S.launches = 0;
@@ -887,7 +889,7 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
 
 void download_shard(fpg_batch* B, ShardBatch& S, bool stats) {
     CK(cudaSetDevice(S.sh->device));
-    cudaStream_t st = S.sh->stream;
+    cudaStream_t st = S.stream;
     const uint64_t nq = B->nq;
     S.h_offsets.reserve(nq + 1);
     S.h_ids.reserve(S.total);
@@ -956,7 +958,7 @@ void upload(fpg_batch* B, const uint8_t* qbytes, const uint64_t* qoffsets, uint6
     for_each_shard(B->sb.size(), [&](size_t i) {
         ShardBatch& S = *B->sb[i];
         CK(cudaSetDevice(S.sh->device));
-        cudaStream_t st = S.sh->stream;
+        cudaStream_t st = S.stream;
         S.qblob.reserve(nbytes + 16);
         S.qoffs.reserve(nq + 1);
         S.qorder.reserve(nq);
@@ -1111,6 +1113,8 @@ void make_batch(fpg_dict* D, fpg_batch** out) {
     for (auto& sh : D->shards) {
         auto S = std::make_unique<ShardBatch>();
         S->sh = sh.get();
+        CK(cudaSetDevice(sh->device));
+        CK(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
         B->sb.push_back(std::move(S));
     }
     *out = B.release();
@@ -1495,20 +1499,23 @@ int fpg_query_batch(fpg_dict* dict, const uint8_t* qbytes, const uint64_t* qoffs
     return guarded([&] {
         if (!dict || !out) throw Error(FPG_EINVAL, "null argument");
         check_opts(dict, opt);
-        // Reuse the dictionary's cached scratch when no other thread holds it.
-        std::unique_lock<std::mutex> lk(dict->cache_mu, std::try_to_lock);
-        std::unique_ptr<fpg_batch> temp;
+        // An idle scratch batch from the dictionary's pool (a new one when all
+        // are busy); concurrent callers get separate batches and streams.
         fpg_batch* b = nullptr;
-        if (lk.owns_lock()) {
-            if (!dict->cached) make_batch(dict, &dict->cached);
-            b = dict->cached;
-        } else {
-            make_batch(dict, &b);
-            temp.reset(b);
+        {
+            std::lock_guard<std::mutex> lk(dict->cache_mu);
+            if (!dict->pool.empty()) {
+                b = dict->pool.back();
+                dict->pool.pop_back();
+            }
         }
+        if (!b) make_batch(dict, &b);
+        std::unique_ptr<fpg_batch> own(b);
         upload(b, qbytes, qoffsets, nq);
         run(b, opt);
         download(b, out);
+        std::lock_guard<std::mutex> lk(dict->cache_mu);
+        if (dict->pool.size() < 16) dict->pool.push_back(own.release());
     });
 }
 
