@@ -689,9 +689,8 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
                 add(lw, qe, (uint32_t)nq, true);
             }
         }
-        // Largest tiles first (the kernel cuts them into warp tiles); the plan
-        // tiles past 60% / 90% of the work are cut to 32 / 16 queries so the
-        // grid drains evenly (FPG_TAIL_A / FPG_TAIL_B).
+        // Largest tiles first; the last ~30% of the work is cut into quarter
+        // tiles so the dynamically scheduled grid drains evenly.
         auto cost = [](const fpg::SliceTile& x) { return (uint64_t)x.q_count * x.n_slabs; };
         std::stable_sort(splan.begin(), splan.end(),
                          [&](const fpg::SliceTile& x, const fpg::SliceTile& y) { return cost(x) > cost(y); });
@@ -699,7 +698,7 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         for (const auto& t : splan) work += cost(t);
         std::vector<fpg::SliceTile> fine;
         fine.reserve(splan.size() + splan.size() / 2);
-        static const double tail_a = env_double("FPG_TAIL_A", 0.6), tail_b = env_double("FPG_TAIL_B", 0.9);
+        static const double tail_a = env_double("FPG_TAIL_A", 0.35), tail_b = env_double("FPG_TAIL_B", 0.85);
         for (const auto& t : splan) {
             acc += cost(t);
             const uint32_t sub = acc <= tail_a * work ? t.q_count : acc <= tail_b * work ? 32u : 16u;

@@ -120,7 +120,7 @@ struct SliceShape {
 // Shared memory of one warp of k_slice<NP, .., S> (npt = NP + S): query
 // masks, query bytes / lengths / ids, candidate queue, verify buffer.
 __host__ __device__ constexpr size_t slice_warp_smem(int npt) {
-    return (size_t)slice_warp_q(npt) * npt * 8 + 44u * slice_warp_q(npt) + 8u * kSliceCap * 32 + 4u * kSliceWarpBuf;
+    return (size_t)slice_warp_q(npt) * npt * 8 + 40u * slice_warp_q(npt) + 8u * kSliceCap * 32 + 4u * kSliceWarpBuf;
 }
 __host__ __device__ constexpr size_t slice_smem_bytes(int npt) { return kSliceWarps * slice_warp_smem(npt); }
 
@@ -139,18 +139,17 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
     uint32_t* s_qid = s_qinfo + WQ;                                        // [WQ]: input query id
     uint2* s_queue = reinterpret_cast<uint2*>(s_qid + WQ);                 // [cap][32 lanes]
     uint32_t* wbuf = reinterpret_cast<uint32_t*>(s_queue + kSliceCap * 32);  // [kSliceWarpBuf]
-    uint32_t* s_wsurv = wbuf + kSliceWarpBuf;                                // [WQ]: fingerprint survivors
     unsigned long long surv_warp = 0;  // lane 0: the warp's fingerprint survivors
     uint32_t cand_lane = 0;
     OutChunk oc;
 
     // Warps are independent: each takes warp tiles (<= WQ queries x 32 SL
     // slabs) from the atomic counter; no CTA-wide barrier anywhere.
-    uint32_t w_next = lane == 0 ? atomicAdd(P.tile_counter, 1u) : 0u;
     for (;;) {
         constexpr uint32_t SUBS = slice_warp_subs(NPT);
-        const uint32_t w = __shfl_sync(0xffffffffu, w_next, 0);
-        if (lane == 0) w_next = atomicAdd(P.tile_counter, 1u);  // the following tile, fetched ahead
+        uint32_t w = 0;
+        if (lane == 0) w = atomicAdd(P.tile_counter, 1u);
+        w = __shfl_sync(0xffffffffu, w, 0);
         const uint32_t t = w / SUBS, sub = w % SUBS;
         if (t >= ntiles) break;
         SliceTile tl = tiles[t];
@@ -184,7 +183,6 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
             s_qb[2 * j + 1] = b1;
             s_qinfo[j] = (uint32_t)m;
             s_qid[j] = id;
-            s_wsurv[j] = 0u;
         }
         // this lane's slabs: tl.slab_begin + lane + 32 r
         uint32_t pl[SL][NPT];
@@ -346,7 +344,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
 #pragma unroll
                     for (int h = 0; h < NQ; ++h) {
                         const uint32_t v = (sv >> (16 * h)) & 0xffffu;
-                        s_wsurv[j + h] += v;
+                        if (v) atomicAdd(&P.q_survivors[s_qid[j + h]], v);
                         surv_warp += v;
                     }
                 }
@@ -386,8 +384,6 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
         if (SL == 2 && tl.n_slabs > 32u) scan_queries(std::integral_constant<int, SL>{});
         else scan_queries(std::integral_constant<int, 1>{});
         if (verify) flush();
-        __syncwarp();
-        if (P.stats && (uint32_t)lane < tl.q_count && s_wsurv[lane]) atomicAdd(&P.q_survivors[s_qid[lane]], s_wsurv[lane]);
         __syncwarp();  // this warp's shared memory is free for the next tile
     }
     if (P.stats && lane == 0 && surv_warp) atomicAdd(P.survivors_total, surv_warp);
