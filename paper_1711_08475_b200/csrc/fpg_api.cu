@@ -560,8 +560,7 @@ void launch_slice(const fpg::SliceTile* tiles, uint32_t ntiles, const fpg::Slice
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, fpg::kSliceThreads, smem));
         resident[dv] = sms * std::max(per_sm, 1);
     }
-    const uint64_t warp_tiles = (uint64_t)ntiles * fpg::slice_warp_subs(NP + S);
-    const uint64_t grid = std::min<uint64_t>(fpg::cdiv_u64(warp_tiles, fpg::kSliceWarps), (uint64_t)resident[dv]);
+    const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)resident[dv]);
     kern<<<(unsigned)std::max<uint64_t>(grid, 1), fpg::kSliceThreads, smem, st>>>(tiles, ntiles, P);
     CK(cudaGetLastError());
 }
@@ -653,7 +652,7 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         // lw; Levenshtein k = 1: lw - 1 .. lw + 1, edit_distance.hpp:38-39).
         // Tiles = (<= 256 SL slabs) x (<= kSliceQ queries), largest first,
         // handed out by an atomic counter.
-        const uint32_t chunk = 32u * fpg::kSliceSlabSubs * fpg::slice_slabs_per_lane(D->npt);
+        const uint32_t chunk = fpg::kSliceThreads * fpg::slice_slabs_per_lane(D->npt);
         const int L1 = fpg::kMaxLen + 1;
         const uint32_t qchunk = fpg::kSliceQ;
         auto add = [&](int lw, uint32_t qb, uint32_t qe, bool count_only) {

@@ -47,14 +47,7 @@ namespace fpg {
 
 constexpr int kSliceThreads = 256;
 constexpr int kSliceWarps = kSliceThreads / 32;
-// A plan tile is <= kSliceQ queries x 256 SL slabs; the kernel cuts it into
-// warp tiles of slice_warp_q queries x 32 SL slabs (kSliceSlabSubs slab
-// chunks x kSliceQ / WQ query chunks), handed to warps by one atomic counter.
-constexpr int kSliceQ = 128;
-constexpr int kSliceSlabSubs = 8;
-// queries per warp tile (shared-memory masks): 32, or 16 when the planes are many
-__host__ __device__ constexpr int slice_warp_q(int npt) { return npt <= 48 ? 32 : 16; }
-__host__ __device__ constexpr int slice_warp_subs(int npt) { return kSliceQ / slice_warp_q(npt) * kSliceSlabSubs; }
+constexpr int kSliceQ = 128;      // queries per tile (shared-memory masks)
 constexpr int kSliceCap = 8;      // queue entries per lane
 constexpr int kSliceWarpBuf = 256;  // expanded candidates per warp and verify round
 
@@ -103,7 +96,6 @@ struct SliceParams {
 };
 
 __device__ __forceinline__ int stride_of_len(int len) { return len <= 16 ? 16 : (len + 15) & ~15; }
-__host__ __device__ constexpr uint64_t cdiv_u64(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
 // x = p XOR (query bit): s = 1, m = 0 keeps p; s = -1, m = ~0 gives ~p.
 __device__ __forceinline__ uint32_t qxor(uint32_t p, uint32_t s, uint32_t m) { return p * s + m; }
@@ -117,54 +109,41 @@ struct SliceShape {
     static_assert(NPT % 2 == 0, "plane pairs");
 };
 
-// Shared memory of one warp of k_slice<NP, .., S> (npt = NP + S): query
-// masks, query bytes / lengths / ids, candidate queue, verify buffer.
-__host__ __device__ constexpr size_t slice_warp_smem(int npt) {
-    return (size_t)slice_warp_q(npt) * npt * 8 + 40u * slice_warp_q(npt) + 8u * kSliceCap * 32 + 4u * kSliceWarpBuf;
+// Dynamic shared memory of k_slice<NP, .., S>.
+__host__ __device__ constexpr size_t slice_smem_bytes(int npt) {
+    return (size_t)kSliceQ * npt * 8 + 32u * kSliceQ + 8u * kSliceQ + 8u * kSliceCap * kSliceThreads +
+           4u * kSliceWarpBuf * kSliceWarps;
 }
-__host__ __device__ constexpr size_t slice_smem_bytes(int npt) { return kSliceWarps * slice_warp_smem(npt); }
 
 template <int NP, int FW, int EXTRA, int S>
-__global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __restrict__ tiles, uint32_t ntiles,  // plan tiles
+__global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __restrict__ tiles, uint32_t ntiles,
                                                             const __grid_constant__ SliceParams P) {
     using Sh = SliceShape<NP, FW, EXTRA, S>;
-    constexpr int NPT = Sh::NPT, SL = Sh::SL, NF = Sh::NF, WQ = slice_warp_q(NPT);
+    constexpr int NPT = Sh::NPT, SL = Sh::SL, NF = Sh::NF;
     extern __shared__ __align__(16) uint8_t smem[];
+    uint2* s_qm = reinterpret_cast<uint2*>(smem);                           // [kSliceQ][NPT] (s, m)
+    uint4* s_qb = reinterpret_cast<uint4*>(s_qm + kSliceQ * NPT);           // [kSliceQ][2]: bytes 0..31
+    uint32_t* s_qinfo = reinterpret_cast<uint32_t*>(s_qb + 2 * kSliceQ);    // [kSliceQ]: length
+    uint32_t* s_qid = s_qinfo + kSliceQ;                                    // [kSliceQ]: input query id
+    uint2* s_queue = reinterpret_cast<uint2*>(s_qid + kSliceQ);             // [cap][threads]
+    uint32_t* s_wbuf = reinterpret_cast<uint32_t*>(s_queue + kSliceCap * kSliceThreads);  // [warps][buf]
+    __shared__ uint32_t s_next[2];  // next tile index, double-buffered by iteration parity
+    __shared__ uint32_t s_surv[kSliceQ];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // this warp's shared memory
-    uint8_t* wsm = smem + (size_t)warp * slice_warp_smem(NPT);
-    uint2* s_qm = reinterpret_cast<uint2*>(wsm);                           // [WQ][NPT] (s, m)
-    uint4* s_qb = reinterpret_cast<uint4*>(s_qm + WQ * NPT);               // [WQ][2]: bytes 0..31
-    uint32_t* s_qinfo = reinterpret_cast<uint32_t*>(s_qb + 2 * WQ);        // [WQ]: length
-    uint32_t* s_qid = s_qinfo + WQ;                                        // [WQ]: input query id
-    uint2* s_queue = reinterpret_cast<uint2*>(s_qid + WQ);                 // [cap][32 lanes]
-    uint32_t* wbuf = reinterpret_cast<uint32_t*>(s_queue + kSliceCap * 32);  // [kSliceWarpBuf]
     unsigned long long surv_warp = 0;  // lane 0: the warp's fingerprint survivors
     uint32_t cand_lane = 0;
     OutChunk oc;
 
-    // Warps are independent: each takes warp tiles (<= WQ queries x 32 SL
-    // slabs) from the atomic counter; no CTA-wide barrier anywhere.
-    for (;;) {
-        constexpr uint32_t SUBS = slice_warp_subs(NPT);
-        uint32_t w = 0;
-        if (lane == 0) w = atomicAdd(P.tile_counter, 1u);
-        w = __shfl_sync(0xffffffffu, w, 0);
-        const uint32_t t = w / SUBS, sub = w % SUBS;
-        if (t >= ntiles) break;
-        SliceTile tl = tiles[t];
-        {   // this warp's part of the plan tile
-            const uint32_t qs = (sub / kSliceSlabSubs) * WQ, ss = (sub % kSliceSlabSubs) * (32u * SL);
-            if (qs >= tl.q_count || ss >= tl.n_slabs) continue;  // empty part of a small tile
-            tl.q_begin += qs;
-            tl.q_count = min(tl.q_count - qs, (uint32_t)WQ);
-            tl.slab_begin += ss;
-            tl.n_slabs = min(tl.n_slabs - ss, 32u * SL);
-        }
+    if (tid == 0) s_next[0] = atomicAdd(P.tile_counter, 1u);
+    __syncthreads();
+    uint32_t t = s_next[0];
+    for (uint32_t it = 1; t < ntiles; ++it) {
+        const SliceTile tl = tiles[t];
+        if (tid == 0) s_next[it & 1] = atomicAdd(P.tile_counter, 1u);  // read after the end-of-tile barrier
 
-        // query (s, m) masks, verifier bytes / lengths / ids; lane j loads query j
-        if ((uint32_t)lane < tl.q_count) {
-            const uint32_t j = (uint32_t)lane, qp = tl.q_begin + j;
+        // query (s, m) masks, verifier bytes / lengths / ids; one query per thread
+        for (uint32_t j = tid; j < tl.q_count; j += kSliceThreads) {
+            const uint32_t qp = tl.q_begin + j;
             const uint64_t f = __ldg(P.q_fp + qp);
             const uint32_t g = __ldg(P.q_sigp + qp);
             const int m = P.q_len[qp];
@@ -183,13 +162,14 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
             s_qb[2 * j + 1] = b1;
             s_qinfo[j] = (uint32_t)m;
             s_qid[j] = id;
+            s_surv[j] = 0u;
         }
-        // this lane's slabs: tl.slab_begin + lane + 32 r
+        // this lane's slabs: tl.slab_begin + tid + 256 r
         uint32_t pl[SL][NPT];
         uint32_t valid[SL];
 #pragma unroll
         for (int r = 0; r < SL; ++r) {
-            const uint32_t rel = (uint32_t)lane + 32u * r;
+            const uint32_t rel = (uint32_t)tid + kSliceThreads * r;
             const uint32_t slab = tl.slab_begin + rel;
             const bool ok = rel < tl.n_slabs;
             const uint32_t* src = P.planes + tl.plane_base + slab;
@@ -198,7 +178,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
             const uint32_t rem = tl.w_count - 32u * slab;  // words left in the bucket from this slab on
             valid[r] = !ok ? 0u : rem >= 32u ? 0xffffffffu : ((1u << rem) - 1u);
         }
-        __syncwarp();
+        __syncthreads();
 
         uint32_t qn = 0;  // queued entries of this lane
         const bool verify = !tl.count_only;
@@ -207,12 +187,13 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
         // mask) entries are first expanded into a warp-wide list of single
         // (query, word) candidates (rounds of <= kSliceWarpBuf), which the 32
         // lanes then verify side by side, one candidate each.
+        uint32_t* wbuf = s_wbuf + warp * kSliceWarpBuf;
         auto flush = [&]() {
             __syncwarp();
             for (;;) {
                 // pending candidate bits of this lane
                 uint32_t c = 0;
-                for (uint32_t s = 0; s < qn; ++s) c += __popc(s_queue[s * 32 + lane].y);
+                for (uint32_t s = 0; s < qn; ++s) c += __popc(s_queue[s * kSliceThreads + tid].y);
                 uint32_t incl = c;
 #pragma unroll
                 for (int d = 1; d < 32; d <<= 1) {
@@ -224,15 +205,15 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 // this lane's candidates take ranks [incl - c, incl); those < kSliceWarpBuf go now
                 uint32_t rank = incl - c;
                 for (uint32_t s = 0; s < qn && rank < (uint32_t)kSliceWarpBuf; ++s) {
-                    uint2 e = s_queue[s * 32 + lane];
+                    uint2 e = s_queue[s * kSliceThreads + tid];
                     const uint32_t j = e.x & 0xffffu, r = e.x >> 16;
-                    const uint32_t wt0 = 32u * ((uint32_t)lane + 32u * r);  // word index within the tile
+                    const uint32_t wt0 = 32u * ((uint32_t)tid + kSliceThreads * r);  // word index within the tile
                     while (e.y && rank < (uint32_t)kSliceWarpBuf) {
                         const int i = __ffs(e.y) - 1;
                         e.y &= e.y - 1;
                         wbuf[rank++] = (j << 16) | (wt0 + (uint32_t)i);
                     }
-                    s_queue[s * 32 + lane].y = e.y;
+                    s_queue[s * kSliceThreads + tid].y = e.y;
                 }
                 __syncwarp();
                 const uint32_t m_all = min(total, (uint32_t)kSliceWarpBuf);
@@ -344,7 +325,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
 #pragma unroll
                     for (int h = 0; h < NQ; ++h) {
                         const uint32_t v = (sv >> (16 * h)) & 0xffffu;
-                        if (v) atomicAdd(&P.q_survivors[s_qid[j + h]], v);
+                        if (v) atomicAdd(&s_surv[j + h], v);
                         surv_warp += v;
                     }
                 }
@@ -365,7 +346,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                     for (int r = 0; r < SLX; ++r) {
                         const uint32_t cand = P.exhaustive ? valid[r] : valid[r] & ~(P.k ? c2[h][r] : c0[h][r]);
                         if (cand) {
-                            s_queue[qn * 32 + lane] = make_uint2((j + h) | ((uint32_t)r << 16), cand);
+                            s_queue[qn * kSliceThreads + tid] = make_uint2((j + h) | ((uint32_t)r << 16), cand);
                             ++qn;
                         }
                     }
@@ -381,10 +362,14 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 for (; j + 2 <= tl.q_count; j += 2) step(slc, std::integral_constant<int, 2>{}, j);
             for (; j < tl.q_count; ++j) step(slc, std::integral_constant<int, 1>{}, j);
         };
-        if (SL == 2 && tl.n_slabs > 32u) scan_queries(std::integral_constant<int, SL>{});
+        if (SL == 2 && 32u * warp + kSliceThreads < tl.n_slabs) scan_queries(std::integral_constant<int, SL>{});
         else scan_queries(std::integral_constant<int, 1>{});
         if (verify) flush();
-        __syncwarp();  // this warp's shared memory is free for the next tile
+        __syncthreads();  // tile consumed; s_next[it & 1] and s_surv complete
+        if (P.stats)
+            for (uint32_t j = tid; j < tl.q_count; j += kSliceThreads)
+                if (s_surv[j]) atomicAdd(&P.q_survivors[s_qid[j]], s_surv[j]);
+        t = s_next[it & 1];
     }
     if (P.stats && lane == 0 && surv_warp) atomicAdd(P.survivors_total, surv_warp);
     oc.close(P.out, P.out_cap);
