@@ -1098,7 +1098,8 @@ void configure_slice(fpg_dict& D, const std::vector<unsigned long long>& hist) {
         if (hist[c] && D.params.slot[c] < 0) others.push_back(c);
     std::stable_sort(others.begin(), others.end(), [&](int a, int b) { return hist[a] > hist[b]; });
     auto snap = [](size_t v) { return v == 0 ? 0 : v <= 8 ? 8 : v <= 12 ? 12 : 16; };
-    int S = snap(others.size());
+    // W = 32 keeps two slabs per lane (NPT <= 40) with at most 8 sig' fields
+    int S = snap(std::min<size_t>(others.size(), D.scheme.width == 32 ? 8 : 16));
     if (const char* sb = std::getenv("FPG_SIGP_BITS")) S = snap((size_t)std::max(0, std::atoi(sb)));
     std::memset(D.params.sigbit, -1, sizeof(D.params.sigbit));
     if (S)

@@ -51,7 +51,7 @@ constexpr int kSliceQ = 128;      // queries per tile (shared-memory masks)
 constexpr int kSliceCap = 8;      // queue entries per lane
 constexpr int kSliceWarpBuf = 256;  // expanded candidates per warp and verify round
 
-__host__ __device__ constexpr int slice_slabs_per_lane(int npt) { return npt <= 32 ? 2 : 1; }
+__host__ __device__ constexpr int slice_slabs_per_lane(int npt) { return npt <= 40 ? 2 : 1; }
 
 struct SliceTile {
     uint32_t slab_begin;   // first slab of the tile, bucket-local
