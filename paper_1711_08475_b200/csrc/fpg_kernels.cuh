@@ -206,16 +206,30 @@ __global__ void __launch_bounds__(256) k_build(const uint8_t* __restrict__ blob,
     if (id_out) id_out[pos] = id;
 }
 
+// Lengths, identity ids and the length histogram (lengths < 256 counted in
+// shared memory first: a dictionary has few distinct lengths, and global
+// atomics on them would serialise).  blockDim == 256.
 __global__ void k_lengths(const uint64_t* __restrict__ offsets, uint64_t n,
                           uint16_t* __restrict__ len_out, uint32_t* __restrict__ idx_out,
                           uint32_t* __restrict__ hist, uint32_t* __restrict__ too_long) {
+    __shared__ uint32_t h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    uint64_t len = offsets[i + 1] - offsets[i];
-    if (len > (uint64_t)kMaxLen) {
-        atomicAdd(too_long, 1u);
-        len = kMaxLen;
+    if (i < n) {
+        uint64_t len = offsets[i + 1] - offsets[i];
+        if (len > (uint64_t)kMaxLen) {
+            atomicAdd(too_long, 1u);
+            len = kMaxLen;
+        }
+        len_out[i] = (uint16_t)len;
+        idx_out[i] = (uint32_t)i;
+        if (len < 256) atomicAdd(&h[len], 1u);
+        else atomicAdd(&hist[len], 1u);
     }
+    __syncthreads();
+    if (h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
+}
     len_out[i] = (uint16_t)len;
     idx_out[i] = (uint32_t)i;
     atomicAdd(&hist[len], 1u);
