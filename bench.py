@@ -293,7 +293,7 @@ def main():
         batch.run(opt, want_stats=True)
     clocks = Clocks(dev)
     clocks.start()
-    run_ms, filt_ms, launches, executed, survivors, candidates = [], [], 0, 0, 0, 0
+    run_ms, filt_ms, launches, executed, survivors, candidates, scanned = [], [], 0, 0, 0, 0, 0
     barrier()
     clocks.open()
     for _ in range(args.steps):
@@ -306,6 +306,7 @@ def main():
         filt_ms.append(t["filter_ms"])
         launches += t["launches"]
         executed, survivors, candidates = t["executed_pairs"], t["survivors"], t["candidates"]
+        scanned = t["scanned_pairs"]
     barrier()
     clocks.close()
     clk = clocks.stop()
@@ -338,13 +339,14 @@ def main():
 
     if rank != 0:
         return
-    # roofline of the dominant kernel (K2): executed (length-compatible) pairs
-    # per launch / the launch's CUDA-event time, against the ALU-pipe bound of
-    # the bit-sliced test
+    # roofline of the dominant kernel (K2): the pairs it evaluated per launch
+    # (length-compatible pairs minus those skipped by the weight window) / the
+    # launch's CUDA-event time, against the ALU-pipe bound of the bit-sliced
+    # test
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     sm_mhz = clk.get("sm_max_mhz") or 1965.0
     filt_avg_ms = statistics.mean(filt_ms)
-    achieved = executed / (filt_avg_ms / 1e3) / 1e12
+    achieved = (scanned or executed) / (filt_avg_ms / 1e3) / 1e12
     shape = d.scan_shape()
     ops = ops_per_comparison(scheme, shape["sig_fields"])
     popc_peak = sms * sm_mhz * 1e6 * POPC_PER_CLK_PER_SM / math.ceil(scheme.width() / 32) / 1e12
@@ -366,7 +368,7 @@ def main():
                    "l2": "flushed between steps (256 MB write)" if flush is not None else "not flushed",
                    "parallelism": f"dict-shard x{world}"},
         "queries_per_s": nq * args.steps / (total_ms / 1e3),
-        "executed_pairs_per_step": executed, "survivors_per_step": survivors,
+        "executed_pairs_per_step": executed, "evaluated_pairs_per_step": scanned, "survivors_per_step": survivors,
         "verifier_candidates_per_step": candidates,
         "matches_per_step": int(csr.offsets[-1]),
         "construction_s": build_s,

@@ -90,6 +90,7 @@ FPG_SIGNATURES = {
                                              ctypes.POINTER(ctypes.c_double), c_u64p, c_u64p,
                                              c_u64p]),
     "fpg_batch_last_candidates": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, c_u64p]),
+    "fpg_batch_last_scanned": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, c_u64p]),
     "fpg_dict_scan_shape": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32),
                                            ctypes.POINTER(ctypes.c_int32)]),
 }

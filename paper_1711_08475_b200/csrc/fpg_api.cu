@@ -71,8 +71,8 @@ int guarded(F&& f) {
 
 inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 // per-run device counters: key slots reserved, survivors, tile counter, verifier
-// candidates, big segment flag, matches
-constexpr int kNumCounters = 6;
+// candidates, big segment flag, matches, pairs evaluated after the weight skip
+constexpr int kNumCounters = 7;
 constexpr unsigned kScatterBlocks = 148 * 4;  // grid-stride K4 scatter (the count is only known on the device)
 inline int stride_of(int len) { return len <= 16 ? 16 : (len + 15) & ~15; }
 
@@ -189,6 +189,12 @@ bool supports(int variant, int metric) {
 
 std::atomic<uint64_t> g_launches{0};  // per process; per-run counts are exact
 
+// FPG_WSKIP=0 turns K2's weight window off (A/B runs)
+const bool g_no_wskip = [] {
+    const char* e = std::getenv("FPG_WSKIP");
+    return e && e[0] == '0';
+}();
+
 const bool g_trace = [] {
     const char* e = std::getenv("FPG_TRACE");
     return e && e[0] == '1';
@@ -227,6 +233,9 @@ struct Collection {
     std::vector<uint32_t> slab_start;    // L1 + 1
     std::vector<uint64_t> plane_base;    // L1
     DBuf<uint32_t> planes;
+    DBuf<uint8_t> wt;         // bit-sliced K2: fingerprint weight per sorted position
+    DBuf<uint16_t> slab_w;    // bit-sliced dictionary: weight range per global slab
+    DBuf<uint32_t> wkey_a, wkey_b;  // scratch: (length << 7 | weight) sort keys
     DBuf<uint32_t> d_slab_start, d_count;
     DBuf<uint64_t> d_plane_base;
     // scratch (len_b = lengths in sorted order; kept for query collections)
@@ -288,17 +297,41 @@ struct Collection {
         int end_bit = 1;
         while ((1 << end_bit) <= max_len) ++end_bit;
         size_t tmp = 0;
-        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, len_a.p, len_b.p, idx_a.p, idx_b.p, (int)n, 0,
-                                           end_bit, st));
-        cub_tmp.reserve(tmp);
-        CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, tmp, len_a.p, len_b.p, idx_a.p, idx_b.p, (int)n, 0,
-                                           end_bit, st));
         const unsigned grid = (unsigned)cdiv(n, 256);
+        if (mode == kSliceDict) {
+            // stable sort by (length, weight): inside a length bucket the words are
+            // ordered by fingerprint weight, so K2 warps see narrow weight ranges
+            wkey_a.reserve(n);
+            wkey_b.reserve(n);
+#define FPG_KEYS(V) fpg::k_weight_keys<V><<<grid, 256, 0, st>>>(d_blob, d_offs, n, P, wkey_a.p)
+            switch (P.variant) {
+                case 0: FPG_KEYS(0); break;
+                case 1: FPG_KEYS(1); break;
+                case 2: FPG_KEYS(2); break;
+                default: FPG_KEYS(3); break;
+            }
+#undef FPG_KEYS
+            CK(cudaGetLastError());
+            ++launches;
+            CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, wkey_a.p, wkey_b.p, idx_a.p, idx_b.p, (int)n, 0,
+                                               end_bit + 7, st));
+            cub_tmp.reserve(tmp);
+            CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, tmp, wkey_a.p, wkey_b.p, idx_a.p, idx_b.p, (int)n, 0,
+                                               end_bit + 7, st));
+            wt.reserve(n);
+        } else {
+            CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, len_a.p, len_b.p, idx_a.p, idx_b.p, (int)n, 0,
+                                               end_bit, st));
+            cub_tmp.reserve(tmp);
+            CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, tmp, len_a.p, len_b.p, idx_a.p, idx_b.p, (int)n, 0,
+                                               end_bit, st));
+        }
         uint64_t* cmp_p = mode == kGenericDict ? cmp.p : nullptr;
         uint32_t* sig_p = mode == kGenericDict ? sig.p : nullptr;
         uint32_t* sigp_p = mode == kGenericDict ? nullptr : sigp.p;
 #define FPG_BUILD(V) fpg::k_build<V><<<grid, 256, 0, st>>>(d_blob, d_offs, idx_b.p, n, d_start.p, d_byte_base.p, P, \
-                                                           fp.p, cmp_p, sig_p, sigp_p, ids.p, bytes.p)
+                                                           fp.p, cmp_p, sig_p, sigp_p, ids.p, bytes.p, nullptr,    \
+                                                           nullptr, nullptr, 0, mode == kSliceDict ? wt.p : nullptr)
         switch (P.variant) {
             case 0: FPG_BUILD(0); break;
             case 1: FPG_BUILD(1); break;
@@ -329,7 +362,9 @@ struct Collection {
             CK(cudaMemcpyAsync(d_slab_start.p, slab_start.data(), sizeof(uint32_t) * (L1 + 1), cudaMemcpyHostToDevice, st));
             CK(cudaMemcpyAsync(d_count.p, count.data(), sizeof(uint32_t) * L1, cudaMemcpyHostToDevice, st));
             CK(cudaMemcpyAsync(d_plane_base.p, plane_base.data(), sizeof(uint64_t) * L1, cudaMemcpyHostToDevice, st));
-            fpg::k_planes<<<(unsigned)cdiv(sl * 32, 256), 256, 0, st>>>(fp.p, sigp.p, d_slab_start.p, d_start.p,
+            slab_w.reserve(sl);
+            fpg::k_planes<<<(unsigned)cdiv(sl * 32, 256), 256, 0, st>>>(fp.p, sigp.p, wt.p, slab_w.p,
+                                                                        d_slab_start.p, d_start.p,
                                                                         d_count.p, d_plane_base.p, L1, (uint32_t)sl,
                                                                         P.width, npt, planes.p);
             CK(cudaGetLastError());
@@ -340,6 +375,7 @@ struct Collection {
 
     void drop_scratch() {
         len_a.release(); len_b.release(); idx_a.release(); idx_b.release(); cub_tmp.release();
+        wkey_a.release(); wkey_b.release();
     }
 
     // Query collection whose length order and bucket tables were built on the
@@ -361,10 +397,15 @@ struct Collection {
         uint64_t* cmp_p = mode == kGenericDict ? cmp.p : nullptr;
         uint32_t* sig_p = mode == kGenericDict ? sig.p : nullptr;
         uint32_t* sigp_p = mode == kGenericDict ? nullptr : sigp.p;
+        uint8_t* wt_p = nullptr;
+        if (mode == kSliceQuery) {
+            wt.reserve(n);
+            wt_p = wt.p;
+        }
         const unsigned grid = (unsigned)std::max<uint64_t>(1, cdiv(n, 256));
 #define FPG_BUILD(V) fpg::k_build<V><<<grid, 256, 0, st>>>(d_blob, d_offs, d_order, n, d_start.p, d_byte_base.p, P, \
                                                            fp.p, cmp_p, sig_p, sigp_p, ids.p, bytes.p, len_b.p,  \
-                                                           zero_by_id, zero64, nzero64)
+                                                           zero_by_id, zero64, nzero64, wt_p)
         switch (P.variant) {
             case 0: FPG_BUILD(0); break;
             case 1: FPG_BUILD(1); break;
@@ -433,7 +474,7 @@ struct ShardBatch {
     HBuf<uint64_t> h_offsets;
     HBuf<uint32_t> h_ids, h_qsurv;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-    uint64_t total = 0, executed = 0, survivors = 0, candidates = 0, launches = 0;
+    uint64_t total = 0, executed = 0, survivors = 0, candidates = 0, scanned = 0, launches = 0;
     double run_ms = 0, filter_ms = 0;
     uint64_t out_cap = 1 << 20;
 };
@@ -673,6 +714,7 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
                     t.w_len = (uint16_t)lw;
                     t.w_stride = (uint16_t)stride_of(lw);
                     t.count_only = count_only ? 1u : 0u;
+                    t.slab_g0 = W.slab_start[lw];
                     splan.push_back(t);
                 }
         };
@@ -779,6 +821,10 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         SP.stats = (o.want_stats && o.use_filter) ? 1 : 0;
         SP.use_fp = supports(D->scheme.variant, o.metric) && !o.exhaustive ? 1 : 0;
         SP.exhaustive = o.exhaustive ? 1 : 0;
+        SP.wskip = SP.use_fp && !o.exhaustive && !g_no_wskip ? 1 : 0;
+        SP.q_weight = Q.wt.p;
+        SP.slab_w = W.slab_w.p;
+        SP.scanned = S.counters.p + 6;
     } else {
         // comparison words: the reference-layout fingerprints when the
         // collections were built for k_slice (no one-hot form, no signatures)
@@ -860,6 +906,7 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
     S.total = S.h_counters.p[5];
     S.survivors = S.h_counters.p[1];
     S.candidates = S.h_counters.p[3];
+    S.scanned = use_slice ? S.h_counters.p[6] : executed;
 
     S.ids_out = S.ids.p;
     if (S.total && (!warp_sort || S.h_counters.p[4])) {
@@ -1496,6 +1543,13 @@ int fpg_batch_last_candidates(const fpg_batch* batch, int32_t shard, uint64_t* c
     return guarded([&] {
         if (!batch || !candidates || shard < 0 || (size_t)shard >= batch->sb.size()) throw Error(FPG_EINVAL, "bad shard");
         *candidates = batch->sb[(size_t)shard]->candidates;
+    });
+}
+
+int fpg_batch_last_scanned(const fpg_batch* batch, int32_t shard, uint64_t* scanned) {
+    return guarded([&] {
+        if (!batch || !scanned || shard < 0 || (size_t)shard >= batch->sb.size()) throw Error(FPG_EINVAL, "bad shard");
+        *scanned = batch->sb[(size_t)shard]->scanned;
     });
 }
 

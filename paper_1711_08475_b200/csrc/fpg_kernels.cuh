@@ -141,6 +141,57 @@ __device__ __forceinline__ uint64_t onehot_count16(uint64_t fp) {
     return r;
 }
 
+// Fingerprint weight: the number of "present" fields (occurrence / halved:
+// set bits; count: non-zero counters; position: letters whose first position
+// is recorded, plus the extra occurrence bits).  One differing field changes
+// it by at most one, so |weight(a) - weight(b)| <= F_D (fingerprint.hpp:171-214):
+// K2 skips query / word groups whose weights differ by more than 2k.
+__device__ __forceinline__ uint32_t fp_weight(uint64_t fp, const SchemeParams& P) {
+    if (P.variant == 0 || P.variant == 1) return (uint32_t)__popcll(fp);
+    const int fw = P.variant == 2 ? P.b : P.p;
+    const int nf = P.variant == 2 ? P.width / P.b : P.slots;
+    const int extra = P.variant == 2 ? 0 : P.extra;
+    const uint64_t fmask = fw >= 64 ? ~0ull : ((1ull << fw) - 1);
+    const uint64_t emask = extra ? ((1ull << extra) - 1) : 0ull;  // position: extra one-bit fields
+    uint32_t w = (uint32_t)__popcll(fp & emask);
+    for (int f = 0; f < nf; ++f) {
+        const uint64_t v = (fp >> (P.width - fw * (f + 1))) & fmask;
+        w += P.variant == 2 ? (v != 0) : (v != fmask);  // position: all-ones = absent
+    }
+    return w;
+}
+
+// Sort keys of the dictionary's K2 layout: (length << 7 | weight) per word in
+// input order (the fingerprint is computed here and again by k_build).
+template <int VARIANT>
+__global__ void __launch_bounds__(256) k_weight_keys(const uint8_t* __restrict__ blob,
+                                                     const uint64_t* __restrict__ offsets, uint64_t n,
+                                                     const __grid_constant__ SchemeParams P,
+                                                     uint32_t* __restrict__ keys) {
+    __shared__ int8_t s_slot[256];
+    s_slot[threadIdx.x] = P.slot[threadIdx.x];
+    __syncthreads();
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t beg = offsets[i];
+    const uint64_t len64 = offsets[i + 1] - beg;
+    const int len = len64 > (uint64_t)kMaxLen ? kMaxLen : (int)len64;
+    FpBuilder<VARIANT> fb;
+    fb.init(P);
+    for (int c = 0; c < len; c += 16) {
+        uint32_t w[4];
+        const int rem = min(16, len - c);
+        load_chunk(blob, beg + c, rem, w);
+#pragma unroll
+        for (int t = 0; t < 16; ++t)
+            if (t < rem) {
+                const int q = s_slot[(w[t >> 2] >> (8 * (t & 3))) & 0xffu];
+                if (q >= 0) fb.add(q, c + t, len, P);
+            }
+    }
+    keys[i] = ((uint32_t)len << 7) | fp_weight(fb.bits, P);
+}
+
 // Inputs: raw blob + offsets, `order` = sorted position -> input index (stable
 // sort by length), per-length bucket tables.  Outputs per sorted position:
 // fingerprint, input id, and the bytes at the bucket's fixed stride (zero
@@ -161,7 +212,7 @@ __global__ void __launch_bounds__(256) k_build(const uint8_t* __restrict__ blob,
                                                uint16_t* __restrict__ len_out = nullptr,
                                                uint32_t* __restrict__ zero_by_id = nullptr,
                                                unsigned long long* __restrict__ zero64 = nullptr,
-                                               int nzero64 = 0) {
+                                               int nzero64 = 0, uint8_t* __restrict__ weight_out = nullptr) {
     __shared__ int8_t s_slot[256];
     __shared__ int8_t s_sigbit[256];
     s_slot[threadIdx.x] = P.slot[threadIdx.x];           // blockDim == 256
@@ -204,6 +255,7 @@ __global__ void __launch_bounds__(256) k_build(const uint8_t* __restrict__ blob,
     if (sig_out) sig_out[pos] = sig;
     if (sigp_out) sigp_out[pos] = sigp;
     if (id_out) id_out[pos] = id;
+    if (weight_out) weight_out[pos] = (uint8_t)fp_weight(fp, P);
 }
 
 // Lengths, identity ids and the length histogram (lengths < 256 counted in
@@ -229,10 +281,6 @@ __global__ void k_lengths(const uint64_t* __restrict__ offsets, uint64_t n,
     }
     __syncthreads();
     if (h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
-}
-    len_out[i] = (uint16_t)len;
-    idx_out[i] = (uint32_t)i;
-    atomicAdd(&hist[len], 1u);
 }
 
 __global__ void k_scatter_prints(const uint64_t* __restrict__ fp, const uint32_t* __restrict__ ids,

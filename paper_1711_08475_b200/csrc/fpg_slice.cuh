@@ -65,7 +65,7 @@ struct SliceTile {
     uint32_t w_count;      // words in the bucket
     uint16_t w_len, w_stride;
     uint32_t count_only;   // fingerprint survivors counted, never verified
-    uint32_t pad;
+    uint32_t slab_g0;      // global index of the bucket's first slab (slab_w)
 };
 
 struct SliceParams {
@@ -92,6 +92,10 @@ struct SliceParams {
     int32_t k;
     int32_t stats;
     int32_t use_fp;             // scheme fields bound this metric (variant_supports, fingerprint.hpp:36-38)
+    int32_t wskip;              // skip query / slab-group pairs whose weights differ by more than 2k
+    const uint8_t* q_weight;    // per sorted query: fingerprint weight (fp_weight)
+    const uint16_t* slab_w;     // per global slab: min | max << 8 of its words' weights
+    unsigned long long* scanned;  // pairs actually evaluated (after the weight skip)
     int32_t exhaustive;         // verify every pair: no fingerprint / sig' pruning (naive-path timing)
 };
 
@@ -112,7 +116,7 @@ struct SliceShape {
 // Dynamic shared memory of k_slice<NP, .., S>.
 __host__ __device__ constexpr size_t slice_smem_bytes(int npt) {
     return (size_t)kSliceQ * npt * 8 + 32u * kSliceQ + 8u * kSliceQ + 8u * kSliceCap * kSliceThreads +
-           4u * kSliceWarpBuf * kSliceWarps;
+           4u * kSliceWarpBuf * kSliceWarps + 2u * kSliceQ * kSliceWarps;
 }
 
 template <int NP, int FW, int EXTRA, int S>
@@ -127,11 +131,14 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
     uint32_t* s_qid = s_qinfo + kSliceQ;                                    // [kSliceQ]: input query id
     uint2* s_queue = reinterpret_cast<uint2*>(s_qid + kSliceQ);             // [cap][threads]
     uint32_t* s_wbuf = reinterpret_cast<uint32_t*>(s_queue + kSliceCap * kSliceThreads);  // [warps][buf]
+    uint16_t* s_qlist = reinterpret_cast<uint16_t*>(s_wbuf + kSliceWarpBuf * kSliceWarps);  // [warps][kSliceQ]
     __shared__ uint32_t s_next[2];  // next tile index, double-buffered by iteration parity
     __shared__ uint32_t s_surv[kSliceQ];
+    __shared__ uint8_t s_qw[kSliceQ];  // query weights
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     unsigned long long surv_warp = 0;  // lane 0: the warp's fingerprint survivors
     uint32_t cand_lane = 0;
+    unsigned long long scanned_warp = 0;  // lane 0
     OutChunk oc;
 
     if (tid == 0) s_next[0] = atomicAdd(P.tile_counter, 1u);
@@ -163,13 +170,18 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
             s_qinfo[j] = (uint32_t)m;
             s_qid[j] = id;
             s_surv[j] = 0u;
+            s_qw[j] = P.wskip ? P.q_weight[qp] : 0;
         }
-        // this lane's slabs: tl.slab_begin + tid + 256 r
+        // this lane's slabs: warp w owns the 32 SL consecutive slabs from
+        // tl.slab_begin + 32 SL w (weights are sorted inside a length bucket,
+        // so a warp's slabs span a narrow weight range); lane l takes slab
+        // 32 r + l of them
         uint32_t pl[SL][NPT];
         uint32_t valid[SL];
+        uint32_t wlo = 0xffu, whi = 0u;  // this lane's slabs' weight range
 #pragma unroll
         for (int r = 0; r < SL; ++r) {
-            const uint32_t rel = (uint32_t)tid + kSliceThreads * r;
+            const uint32_t rel = 32u * SL * warp + 32u * r + (uint32_t)lane;
             const uint32_t slab = tl.slab_begin + rel;
             const bool ok = rel < tl.n_slabs;
             const uint32_t* src = P.planes + tl.plane_base + slab;
@@ -177,6 +189,11 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
             for (int b = 0; b < NPT; ++b) pl[r][b] = ok ? __ldg(src + (size_t)b * tl.ns) : 0u;
             const uint32_t rem = tl.w_count - 32u * slab;  // words left in the bucket from this slab on
             valid[r] = !ok ? 0u : rem >= 32u ? 0xffffffffu : ((1u << rem) - 1u);
+            if (ok && P.wskip) {
+                const uint32_t mm = __ldg(P.slab_w + tl.slab_g0 + slab);
+                wlo = min(wlo, mm & 0xffu);
+                whi = max(whi, mm >> 8);
+            }
         }
         __syncthreads();
 
@@ -207,7 +224,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 for (uint32_t s = 0; s < qn && rank < (uint32_t)kSliceWarpBuf; ++s) {
                     uint2 e = s_queue[s * kSliceThreads + tid];
                     const uint32_t j = e.x & 0xffffu, r = e.x >> 16;
-                    const uint32_t wt0 = 32u * ((uint32_t)tid + kSliceThreads * r);  // word index within the tile
+                    const uint32_t wt0 = 32u * (32u * SL * warp + 32u * r + (uint32_t)lane);  // word index within the tile
                     while (e.y && rank < (uint32_t)kSliceWarpBuf) {
                         const int i = __ffs(e.y) - 1;
                         e.y &= e.y - 1;
@@ -270,12 +287,18 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
         // bucket's last chunk) run the one-slab loop instead of scanning zeros.
         // One step = NQ consecutive queries (j .. j + NQ - 1) against the
         // lane's SLX slabs: NQ * SLX independent counter chains per plane.
-        auto step = [&](auto slc, auto nqc, uint32_t j) {
+        // step over list entries i .. i + NQ - 1 (tile query indices)
+        const uint16_t* qlist = s_qlist + warp * kSliceQ;
+        auto step = [&](auto slc, auto nqc, uint32_t i) {
             constexpr int SLX = decltype(slc)::value;
             constexpr int NQ = decltype(nqc)::value;
             const uint4* qm[NQ];
+            uint32_t jq[NQ];
 #pragma unroll
-            for (int h = 0; h < NQ; ++h) qm[h] = reinterpret_cast<const uint4*>(s_qm + (j + h) * NPT);
+            for (int h = 0; h < NQ; ++h) {
+                jq[h] = qlist[i + h];
+                qm[h] = reinterpret_cast<const uint4*>(s_qm + jq[h] * NPT);
+            }
             uint32_t c0[NQ][SLX], c1[NQ][SLX], c2[NQ][SLX];
 #pragma unroll
             for (int h = 0; h < NQ; ++h)
@@ -325,7 +348,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
 #pragma unroll
                     for (int h = 0; h < NQ; ++h) {
                         const uint32_t v = (sv >> (16 * h)) & 0xffffu;
-                        if (v) atomicAdd(&s_surv[j + h], v);
+                        if (v) atomicAdd(&s_surv[jq[h]], v);
                         surv_warp += v;
                     }
                 }
@@ -346,7 +369,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                     for (int r = 0; r < SLX; ++r) {
                         const uint32_t cand = P.exhaustive ? valid[r] : valid[r] & ~(P.k ? c2[h][r] : c0[h][r]);
                         if (cand) {
-                            s_queue[qn * kSliceThreads + tid] = make_uint2((j + h) | ((uint32_t)r << 16), cand);
+                            s_queue[qn * kSliceThreads + tid] = make_uint2(jq[h] | ((uint32_t)r << 16), cand);
                             ++qn;
                         }
                     }
@@ -356,13 +379,40 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
 #undef FPG_QM
 #undef FPG_CNT
         };
+        // This warp's queries: those whose weight is within 2k of its slabs'
+        // weight range (the others have F_D > 2k with every word here:
+        // |weight difference| <= F_D), compacted into a list.
+        uint32_t nlist = 0;
+        {
+            const uint32_t lo = __reduce_min_sync(0xffffffffu, wlo), hi = __reduce_max_sync(0xffffffffu, whi);
+            const uint32_t span = 2u * (uint32_t)P.k;
+            uint16_t* ql = s_qlist + warp * kSliceQ;
+            for (uint32_t b = 0; b < tl.q_count; b += 32) {
+                const uint32_t j = b + (uint32_t)lane;
+                bool in = j < tl.q_count;
+                if (in && P.wskip) {
+                    const uint32_t w = s_qw[j];
+                    in = w + span >= lo && w <= hi + span;
+                }
+                const uint32_t bal = __ballot_sync(0xffffffffu, in);
+                if (in) ql[nlist + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)j;
+                nlist += __popc(bal);
+            }
+            __syncwarp();
+            // pairs actually evaluated by this warp (stats / roofline)
+            uint32_t vw = 0;
+#pragma unroll
+            for (int r = 0; r < SL; ++r) vw += __popc(valid[r]);
+            vw = __reduce_add_sync(0xffffffffu, vw);
+            if (lane == 0 && verify) scanned_warp += (unsigned long long)vw * nlist;
+        }
         auto scan_queries = [&](auto slc) {
-            uint32_t j = 0;
+            uint32_t i = 0;
             if constexpr (NPT <= 48)  // query pairs while the registers allow it
-                for (; j + 2 <= tl.q_count; j += 2) step(slc, std::integral_constant<int, 2>{}, j);
-            for (; j < tl.q_count; ++j) step(slc, std::integral_constant<int, 1>{}, j);
+                for (; i + 2 <= nlist; i += 2) step(slc, std::integral_constant<int, 2>{}, i);
+            for (; i < nlist; ++i) step(slc, std::integral_constant<int, 1>{}, i);
         };
-        if (SL == 2 && 32u * warp + kSliceThreads < tl.n_slabs) scan_queries(std::integral_constant<int, SL>{});
+        if (SL == 2 && 32u * SL * warp + 32u < tl.n_slabs) scan_queries(std::integral_constant<int, SL>{});
         else scan_queries(std::integral_constant<int, 1>{});
         if (verify) flush();
         __syncthreads();  // tile consumed; s_next[it & 1] and s_surv complete
@@ -374,6 +424,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
     if (P.stats && lane == 0 && surv_warp) atomicAdd(P.survivors_total, surv_warp);
     oc.close(P.out, P.out_cap);
     if (lane == 0 && oc.real) atomicAdd(P.match_total, (unsigned long long)oc.real);
+    if (lane == 0 && scanned_warp) atomicAdd(P.scanned, scanned_warp);
     cand_lane = __reduce_add_sync(0xffffffffu, cand_lane);
     if (lane == 0 && cand_lane) atomicAdd(P.candidates, (unsigned long long)cand_lane);
 }
@@ -382,6 +433,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
 // One warp per slab: lane i holds word 32 s + i of its bucket; plane b is the
 // ballot of bit b of the words' codes (fingerprint bits, then sig' bits).
 __global__ void k_planes(const uint64_t* __restrict__ fp, const uint32_t* __restrict__ sigp,
+                         const uint8_t* __restrict__ weight, uint16_t* __restrict__ slab_w,
                          const uint32_t* __restrict__ slab_start,  // per length: first global slab (L1 + 1)
                          const uint32_t* __restrict__ start,       // per length: first sorted position
                          const uint32_t* __restrict__ count,       // per length: words
@@ -403,6 +455,12 @@ __global__ void k_planes(const uint64_t* __restrict__ fp, const uint32_t* __rest
     const bool ok = w < count[L];
     const uint64_t f = ok ? fp[start[L] + w] : 0ull;
     const uint32_t g = ok ? sigp[start[L] + w] : 0u;
+    if (slab_w) {  // the slab's weight range (K2's weight window)
+        const uint32_t wt = ok ? weight[start[L] + w] : 0u;
+        const uint32_t lo = __reduce_min_sync(0xffffffffu, ok ? wt : 0xffu);
+        const uint32_t hi = __reduce_max_sync(0xffffffffu, ok ? wt : 0u);
+        if (lane == 0) slab_w[gs] = (uint16_t)(lo | (hi << 8));
+    }
     uint32_t mine[3] = {0u, 0u, 0u};
 #pragma unroll
     for (int r = 0; r < 3; ++r) {

@@ -542,10 +542,11 @@ class Batch:
         ex, sv, ln = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
         check(self._lib.fpg_batch_last_timing(self._h, shard, ctypes.byref(run_ms), ctypes.byref(filt_ms),
                                               ctypes.byref(ex), ctypes.byref(sv), ctypes.byref(ln)))
-        cand = ctypes.c_uint64()
+        cand, scan = ctypes.c_uint64(), ctypes.c_uint64()
         check(self._lib.fpg_batch_last_candidates(self._h, shard, ctypes.byref(cand)))
+        check(self._lib.fpg_batch_last_scanned(self._h, shard, ctypes.byref(scan)))
         return {"run_ms": run_ms.value, "filter_ms": filt_ms.value, "executed_pairs": ex.value,
-                "survivors": sv.value, "launches": ln.value, "candidates": cand.value}
+                "survivors": sv.value, "launches": ln.value, "candidates": cand.value, "scanned_pairs": scan.value}
 
     def close(self) -> None:
         if getattr(self, "_h", None):

@@ -1,3 +1,4 @@
+# GPU tests + short bench runs of the given config_cell specs (e.g. 2_0 5_0).
 mkdir -p gpurun_out/sweep
 timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pt.log 2>&1; echo pytest_rc=$?; tail -2 gpurun_out/pt.log
 for spec in "$@"; do
@@ -6,6 +7,6 @@ for spec in "$@"; do
   echo "cfg=$cfg cell=$cell rc=$? $(tail -1 gpurun_out/sweep/c${cfg}_${cell}.log | python -c 'import sys,json
 try:
   d=json.loads(sys.stdin.read()); r=d["roofline"]
-  print(d["config"]["cell"], "step_ms=%.3f" % d["ms_per_step"], "k2_ms=%.3f" % r["filter_ms_per_launch"], "Tcmp/s=%.2f" % r["achieved"], "frac=%.2f" % r["frac"], "popc_frac=%.2f" % r["popc_equiv_frac"], "e2e=%.3g" % d["e2e"]["value"], "matches=%d" % d["matches_per_step"], "cand=%d" % d["verifier_candidates_per_step"])
+  print(d["config"]["cell"], "step_ms=%.3f" % d["ms_per_step"], "k2_ms=%.3f" % r["filter_ms_per_launch"], "Tcmp/s=%.2f" % r["achieved"], "frac=%.2f" % r["frac"], "eval/exec=%.3f" % (d["evaluated_pairs_per_step"] / max(1, d["executed_pairs_per_step"])), "e2e=%.3g" % d["e2e"]["value"], "matches=%d" % d["matches_per_step"], "cand=%d" % d["verifier_candidates_per_step"])
 except Exception as e: print("parse error", e)')"
 done
