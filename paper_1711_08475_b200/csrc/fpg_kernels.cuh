@@ -358,12 +358,23 @@ __global__ void k_seg_scatter(const unsigned long long* __restrict__ keys, const
     const uint64_t used = *slots;
     const uint64_t n = used < cap ? used : cap;  // overflowed runs are redone by the host
     const uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
     if (i0 == 0) *offsets_last = *matches;
-    for (uint64_t i = i0; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const unsigned long long k = keys[i];
+    // warp-uniform trip count; lanes holding keys of the same query claim
+    // their slots with one atomic (popular queries would serialise otherwise)
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t b = i0 - lane; b < n; b += stride) {
+        const uint64_t i = b + lane;
+        const unsigned long long k = i < n ? keys[i] : kNoKey;
+        const uint32_t q = (uint32_t)(k >> 32);  // kNoKey -> 0xffffffff, never a query
+        const uint32_t peers = __match_any_sync(0xffffffffu, q);
         if (k == kNoKey) continue;
-        const uint32_t q = (uint32_t)(k >> 32);
-        const uint64_t pos = offsets_in[q] + (atomicSub(&cursor[q], 1u) - 1u);
+        const int leader = __ffs(peers) - 1;
+        const uint32_t cnt = (uint32_t)__popc(peers);
+        uint32_t base = 0;
+        if (lane == leader) base = atomicSub(&cursor[q], cnt) - cnt;
+        base = __shfl_sync(peers, base, leader);
+        const uint64_t pos = offsets_in[q] + base + (uint32_t)__popc(peers & ((1u << lane) - 1u));
         if (pos < cap) ids[pos] = (uint32_t)k;
     }
 }
