@@ -693,12 +693,33 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         // lw; Levenshtein k = 1: lw - 1 .. lw + 1, edit_distance.hpp:38-39).
         // Tiles = (<= 256 SL slabs) x (<= kSliceQ queries), largest first,
         // handed out by an atomic counter.
-        const uint32_t chunk = fpg::kSliceThreads * fpg::slice_slabs_per_lane(D->npt);
         const int L1 = fpg::kMaxLen + 1;
-        const uint32_t qchunk = fpg::kSliceQ;
+        // Tile shape: 128 queries x 256 SL slabs, made smaller (queries down to
+        // 16, then slabs down to one warp's 32 SL) while a small batch would give
+        // fewer than ~4 tiles per resident CTA.
+        const uint32_t sl = (uint32_t)fpg::slice_slabs_per_lane(D->npt);
+        uint32_t per = fpg::kSliceThreads * sl, qchunk = fpg::kSliceQ;
+        {
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, sh.device);
+            const uint64_t target = (uint64_t)sms * 2 * 4;
+            auto count_tiles = [&]() {
+                uint64_t c = 0;
+                for (int lw = 0; lw <= W.max_len; ++lw) {
+                    if (!W.count[lw]) continue;
+                    const int span = (o.metric == FPG_HAMMING) ? 0 : o.k;
+                    const int lo = std::max(0, lw - span), hi = std::min(L1 - 1, lw + span);
+                    c += cdiv(Q.start[hi] + Q.count[hi] - Q.start[lo], qchunk) * cdiv(cdiv(W.count[lw], 32), per);
+                }
+                return c;
+            };
+            while (count_tiles() < target && (qchunk > 16 || per > 32u * sl)) {
+                if (qchunk > 16) qchunk >>= 1;
+                else per >>= 1;
+            }
+        }
         auto add = [&](int lw, uint32_t qb, uint32_t qe, bool count_only) {
             const uint32_t ns = (uint32_t)cdiv(W.count[lw], 32);
-            const uint32_t per = chunk;
             for (uint32_t q0 = qb; q0 < qe; q0 += qchunk)
                 for (uint32_t s0 = 0; s0 < ns; s0 += per) {
                     fpg::SliceTile t{};
