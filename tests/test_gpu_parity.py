@@ -363,3 +363,26 @@ def test_dictionary_from_text_config(oracle):
         assert d.size() == len(words)
         csr, st = d.query_batch((qblob, qoffs), QueryOptions(Metric.Levenshtein, 1, True, True), True)
     assert_same(csr, st, *oracle.query_batch(blob, offs, qblob, qoffs, osch(s), Metric.Levenshtein, 1, True, True))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg,cell,nsample", [(3, 0, 40), (3, 1, 40), (4, 0, 40), (4, 1, 40), (5, 0, 40), (5, 5, 40)])
+def test_full_size_configs_vs_oracle(oracle, cfg, cell, nsample):
+    """BASELINE sizes (config 3: 2e6 words x 5e4 queries, config 4: 8e6 x 1e5,
+    config 5: 6.4e7 x 1e6 on one GPU): the whole batch runs on the GPU; an
+    evenly spaced query subsample is checked against the oracle (ids and
+    QueryStats), plus the batch total against the filter-off run."""
+    import bench
+    from paper_1711_08475_b200.corpus import CELLS
+
+    c, blob, offs, qblob, qoffs, scheme, metric, first, n = bench.workload(cfg, cell, 0, 1)
+    nq = len(qoffs) - 1
+    opt = QueryOptions(metric, 1, True, True)
+    with GpuFingerprintedDictionary((blob, offs), scheme, keep_words=False) as d:
+        csr, st = d.query_batch((qblob, qoffs), opt, per_query_stats=True)
+    sb, so, idx = subsample(qblob, qoffs, max(1, nq // nsample))
+    o_off, o_ids, o_st = oracle.query_batch(blob, offs, sb, so, osch(scheme), metric, 1, True, True)
+    for j, q in enumerate(idx):
+        assert np.array_equal(csr.row(q), o_ids[int(o_off[j]):int(o_off[j + 1])]), f"query {q}"
+        assert np.array_equal(st[q], o_st[j]), f"stats of query {q}"
+    assert int(st[:, 4].sum()) == len(csr.word_ids)
