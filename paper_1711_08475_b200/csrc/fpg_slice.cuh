@@ -1,7 +1,8 @@
 // fpg_slice.cuh -- K2 as a bit-sliced scan (sm_100a): no POPC on the pair path.
 //
-// Layout.  The words of one dictionary length bucket are cut into slabs of 32
-// consecutive (input-ordered) words.  A slab is stored as NPT 32-bit planes:
+// Layout.  The words of one dictionary length bucket, sorted by fingerprint
+// weight (input order within a weight), are cut into slabs of 32 consecutive
+// words.  A slab is stored as NPT 32-bit planes:
 // plane b holds bit b of the 32 words' comparison codes (K1b k_planes).
 // Planes 0..NP-1 are the scheme fingerprint bits in the reference layout
 // (fingerprint.hpp:48-56, :138-147: NF fields of FW bits above EXTRA one-bit
@@ -21,10 +22,14 @@
 //                                           counters, c_i = "F >= i+1" per word
 // so bit w of c2 (c0 for k = 0) says word w is rejected.  Per 32 pairs that
 // is 3 ALU ops per 1-bit field (4 per wider field) and one IMAD per plane:
-// about 1.0-1.5 ALU ops per comparison at W = 16, against the POPC pipe's
-// 16/clk/SM bound of a per-pair XOR + POPC.
+// 1.0-1.5 ALU ops per comparison for a 16-bit fingerprint, against the POPC
+// pipe's 16/clk/SM bound of a per-pair XOR + POPC.
 //
-// sig' (internal, exact).  Bytes that are NOT scheme letters are hashed into S
+// Weight window.  |weight(q) - weight(x)| <= F_D (fp_weight), so a warp skips
+// the queries whose weight is more than 2k away from its slabs' range: those
+// pairs are rejected by the reference test anyway.
+//
+// sig' (internal, exact).  Bytes that are NOT scheme letters are dealt into S
 // extra one-bit occurrence fields (host LUT, frequency round robin).  One edit
 // involves at most two symbols and each symbol owns at most one field of
 // (scheme fields + sig' fields), so F_D + F_sig' <= 2 * distance for every
@@ -36,8 +41,9 @@
 //
 // Candidates (rare) go to a lane-private queue in shared memory as
 // (query, slab, 32-bit word mask) and are byte-verified at k <= 1
-// (edit_distance.hpp:18-64) in batches; matches leave through a
-// warp-aggregated atomic append as (query id << 32 | word id) keys for K4.
+// (edit_distance.hpp:18-64) in warp-wide batches; matches leave as
+// (query id << 32 | word id) keys through per-warp output chunks (OutChunk)
+// for K4.
 #pragma once
 
 #include <cstdint>
