@@ -2,11 +2,12 @@
 //
 // Host runtime: per-device shards of the dictionary (contiguous input-order
 // id ranges, dictionary.hpp:51-56 keeps input order), per-batch device
-// scratch, tile planning over (query length, word length) bucket pairs, and
-// the host-side CSR merge across shards.  No compute happens on the host:
-// fingerprints, filtering, verification, ordering and CSR construction all
-// run on the GPU; the host only plans tiles from bucket counts, turns the
-// per-query survivor counts into QueryStats and concatenates shard rows.
+// scratch and streams, tile planning over length buckets, and the host-side
+// CSR merge across shards.  No compute happens on the host: fingerprints,
+// filtering, verification, ordering and CSR construction all run on the GPU;
+// the host only counting-sorts query lengths, plans tiles from bucket
+// counts, turns the per-query survivor counts into QueryStats and
+// concatenates shard rows.
 #include <cuda_runtime.h>
 
 #include <algorithm>

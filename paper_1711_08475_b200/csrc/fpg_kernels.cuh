@@ -1,18 +1,18 @@
-// fpg_kernels.cuh -- sm_100a kernels of the fingerprint-filtered k<=1 scan.
+// fpg_kernels.cuh -- sm_100a kernels of the fingerprint-filtered k-approximate scan.
 //
+//   K0 k_hist256    byte histogram (sig' ranking, letter selection)
 //   K1 k_build      one thread per string: fingerprint (reference build(),
-//                   fingerprint.hpp:216-284, generalised to W bits) + copy of
-//                   the bytes into the length-bucketed, 16-byte-stride layout.
-//   K2 k_scan       query x word tiles of one (query length, word length)
-//                   bucket pair: XOR + POPC fingerprint test
-//                   (dictionary.hpp:102-106; ComparisonTables::distance
-//                   fingerprint.hpp:171-214) for every pair, survivors
-//                   compacted per warp with __ballot_sync into shared memory
-//                   and verified there at k<=1 (edit_distance.hpp:18-64),
-//                   matches appended with warp-aggregated atomics.
+//                   fingerprint.hpp:216-284, generalised to W bits), sig'
+//                   code, weight, and the bytes copied into the length-bucketed
+//                   16-byte-stride layout.  k_weight_keys / k_lengths feed the
+//                   (length, weight) sort of the dictionary.
+//   K1b k_planes    bit-sliced planes per 32-word slab (fpg_slice.cuh)
+//   K2 k_slice      the bit-sliced filter + k <= 1 verifier (fpg_slice.cuh);
+//      k_scan       the generic per-pair XOR + POPC filter (fpg_scan.cuh):
+//                   fields wider than 4 bits, k >= 2 (banded verifier)
 //   K4 k_seg_scatter / k_seg_sort   CSR: keys scattered into per-query
-//                   segments, small segments warp-sorted (large ones: CUB
-//                   segmented sort on the host side of the launch).
+//                   segments, segments of <= 32 warp-sorted (larger ones: CUB
+//                   segmented sort, launched by the host)
 #pragma once
 
 #include <cstdint>
