@@ -109,6 +109,8 @@ __device__ __forceinline__ int stride_of_len(int len) { return len <= 16 ? 16 : 
 
 // x = p XOR (query bit): s = 1, m = 0 keeps p; s = -1, m = ~0 gives ~p.
 __device__ __forceinline__ uint32_t qxor(uint32_t p, uint32_t s, uint32_t m) { return p * s + m; }
+// bitwise majority (the carry of a full adder): one LOP3
+__device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (c & (a | b)); }
 
 template <int NP, int FW, int EXTRA, int S>
 struct SliceShape {
@@ -305,50 +307,78 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 jq[h] = qlist[i + h];
                 qm[h] = reinterpret_cast<const uint4*>(s_qm + jq[h] * NPT);
             }
-            uint32_t c0[NQ][SLX], c1[NQ][SLX], c2[NQ][SLX];
+            // Carry-save saturating counter per word: F = o + 2 t + 4 [f], i.e.
+            // o = ones bit, t = twos bit, f = "F >= 4".  Field bits enter four
+            // at a time (two full adders into o, one into t: 7 LOP3 per 4
+            // fields) or two at a time (4 LOP3); reject at k = 1 is
+            // F >= 3 = f | (t & o), at k = 0 F >= 1 = f | t | o.
+            uint32_t co[NQ][SLX], ct[NQ][SLX], cf[NQ][SLX];
 #pragma unroll
             for (int h = 0; h < NQ; ++h)
 #pragma unroll
-                for (int r = 0; r < SLX; ++r) c0[h][r] = c1[h][r] = c2[h][r] = 0u;
+                for (int r = 0; r < SLX; ++r) co[h][r] = ct[h][r] = cf[h][r] = 0u;
             // (s, m) of plane b for query h
 #define FPG_QS(h, b) ((b) & 1 ? qm[h][(b) >> 1].z : qm[h][(b) >> 1].x)
 #define FPG_QM(h, b) ((b) & 1 ? qm[h][(b) >> 1].w : qm[h][(b) >> 1].y)
-#define FPG_CNT(h, r, x)            \
-    do {                              \
-        c2[h][r] |= c1[h][r] & (x);   \
-        c1[h][r] |= c0[h][r] & (x);   \
-        c0[h][r] |= (x);              \
-    } while (0)
-            // scheme fields: NF fields of FW planes above EXTRA one-bit fields.
-            // Skipped when they do not bound the metric (halved / position with
-            // Levenshtein, filter off): sig' alone stays a valid bound.
-            if (P.use_fp) {
+            // field i of the code as a 32-word "differs" mask: scheme fields
+            // (NF fields of FW planes, then EXTRA one-bit fields), then sig'
+            auto fbit = [&](int h, int r, int i) -> uint32_t {
+                if (i < NF) {
+                    const int b0 = EXTRA + FW * i;
+                    uint32_t x = qxor(pl[r][b0], FPG_QS(h, b0), FPG_QM(h, b0));
 #pragma unroll
-                for (int f = 0; f < NF; ++f) {
-                    const int b0 = EXTRA + FW * f;
-#pragma unroll
-                    for (int h = 0; h < NQ; ++h)
-#pragma unroll
-                        for (int r = 0; r < SLX; ++r) {
-                            uint32_t x = qxor(pl[r][b0], FPG_QS(h, b0), FPG_QM(h, b0));
-#pragma unroll
-                            for (int u = 1; u < FW; ++u) x |= qxor(pl[r][b0 + u], FPG_QS(h, b0 + u), FPG_QM(h, b0 + u));
-                            FPG_CNT(h, r, x);
-                        }
+                    for (int u = 1; u < FW; ++u) x |= qxor(pl[r][b0 + u], FPG_QS(h, b0 + u), FPG_QM(h, b0 + u));
+                    return x;
                 }
+                const int b = i < NF + EXTRA ? i - NF : NP + (i - NF - EXTRA);
+                return qxor(pl[r][b], FPG_QS(h, b), FPG_QM(h, b));
+            };
+            auto add4 = [&](int h, int r, uint32_t x1, uint32_t x2, uint32_t x3, uint32_t x4) {
+                const uint32_t o = co[h][r];
+                const uint32_t o1 = o ^ x1 ^ x2, k1 = maj3(o, x1, x2);
+                const uint32_t k2 = maj3(o1, x3, x4);
+                co[h][r] = o1 ^ x3 ^ x4;
+                const uint32_t t = ct[h][r];
+                cf[h][r] |= maj3(t, k1, k2);
+                ct[h][r] = t ^ k1 ^ k2;
+            };
+            auto add2 = [&](int h, int r, uint32_t x1, uint32_t x2) {
+                const uint32_t o = co[h][r], k1 = maj3(o, x1, x2);
+                co[h][r] = o ^ x1 ^ x2;
+                cf[h][r] |= ct[h][r] & k1;
+                ct[h][r] ^= k1;
+            };
+            // fields [i0, i1) into the counters
+            auto count = [&](auto i0c, auto i1c) {
+                constexpr int I0 = decltype(i0c)::value, I1 = decltype(i1c)::value;
+                constexpr int N4 = (I1 - I0) / 4 * 4;
 #pragma unroll
-                for (int e = 0; e < EXTRA; ++e)
+                for (int i = I0; i < I0 + N4; i += 4)
 #pragma unroll
                     for (int h = 0; h < NQ; ++h)
 #pragma unroll
-                        for (int r = 0; r < SLX; ++r) FPG_CNT(h, r, qxor(pl[r][e], FPG_QS(h, e), FPG_QM(h, e)));
-            }
+                        for (int r = 0; r < SLX; ++r)
+                            add4(h, r, fbit(h, r, i), fbit(h, r, i + 1), fbit(h, r, i + 2), fbit(h, r, i + 3));
+#pragma unroll
+                for (int i = I0 + N4; i < I1; i += 2)
+#pragma unroll
+                    for (int h = 0; h < NQ; ++h)
+#pragma unroll
+                        for (int r = 0; r < SLX; ++r) add2(h, r, fbit(h, r, i), i + 1 < I1 ? fbit(h, r, i + 1) : 0u);
+            };
+            auto rejected = [&](int h, int r) -> uint32_t {
+                return P.k ? cf[h][r] | (ct[h][r] & co[h][r]) : cf[h][r] | ct[h][r] | co[h][r];
+            };
+            // scheme fields.  Skipped when they do not bound the metric (halved
+            // / position with Levenshtein, filter off): sig' alone stays a
+            // valid bound.
+            if (P.use_fp) count(std::integral_constant<int, 0>{}, std::integral_constant<int, NF + EXTRA>{});
             if (P.stats) {  // fingerprint survivors: QueryStats::verified (dictionary.hpp:102-110)
                 uint32_t sv = 0;  // query h in bits [16 h, 16 h + 16): <= 2048 per warp
 #pragma unroll
                 for (int h = 0; h < NQ; ++h)
 #pragma unroll
-                    for (int r = 0; r < SLX; ++r) sv += (uint32_t)__popc(valid[r] & ~(P.k ? c2[h][r] : c0[h][r])) << (16 * h);
+                    for (int r = 0; r < SLX; ++r) sv += (uint32_t)__popc(valid[r] & ~rejected(h, r)) << (16 * h);
                 sv = __reduce_add_sync(0xffffffffu, sv);
                 if (lane == 0) {
 #pragma unroll
@@ -360,20 +390,13 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 }
             }
             if (verify) {
-                if (!P.exhaustive) {
-#pragma unroll
-                    for (int g = 0; g < S; ++g)
-#pragma unroll
-                        for (int h = 0; h < NQ; ++h)
-#pragma unroll
-                            for (int r = 0; r < SLX; ++r)
-                                FPG_CNT(h, r, qxor(pl[r][NP + g], FPG_QS(h, NP + g), FPG_QM(h, NP + g)));
-                }
+                if (!P.exhaustive)
+                    count(std::integral_constant<int, NF + EXTRA>{}, std::integral_constant<int, NF + EXTRA + S>{});
 #pragma unroll
                 for (int h = 0; h < NQ; ++h)
 #pragma unroll
                     for (int r = 0; r < SLX; ++r) {
-                        const uint32_t cand = P.exhaustive ? valid[r] : valid[r] & ~(P.k ? c2[h][r] : c0[h][r]);
+                        const uint32_t cand = P.exhaustive ? valid[r] : valid[r] & ~rejected(h, r);
                         if (cand) {
                             s_queue[qn * kSliceThreads + tid] = make_uint2(jq[h] | ((uint32_t)r << 16), cand);
                             ++qn;
@@ -383,7 +406,6 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
             }
 #undef FPG_QS
 #undef FPG_QM
-#undef FPG_CNT
         };
         // This warp's queries: those whose weight is within 2k of its slabs'
         // weight range (the others have F_D > 2k with every word here:
