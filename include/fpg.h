@@ -165,8 +165,9 @@ int fpg_dict_scan_shape(const fpg_dict* dict, int32_t* sliced, int32_t* sig_fiel
  * the fingerprint test and the verifier's own exact pre-filters). */
 int fpg_batch_last_candidates(const fpg_batch* batch, int32_t shard, uint64_t* candidates);
 /* Length-compatible pairs the last run on `shard` actually evaluated: the
- * executed pairs minus those skipped whole because their fingerprint weights
- * differ by more than 2k (|weight difference| <= F_D, so they are rejected). */
+ * executed pairs minus those skipped whole because their group weights are
+ * more than 2k apart (L1 distance over 4 field groups <= F_D, so they are
+ * rejected). */
 int fpg_batch_last_scanned(const fpg_batch* batch, int32_t shard, uint64_t* scanned);
 
 #ifdef __cplusplus

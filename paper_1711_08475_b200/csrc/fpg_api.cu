@@ -234,9 +234,9 @@ struct Collection {
     std::vector<uint32_t> slab_start;    // L1 + 1
     std::vector<uint64_t> plane_base;    // L1
     DBuf<uint32_t> planes;
-    DBuf<uint8_t> wt;         // bit-sliced K2: fingerprint weight per sorted position
-    DBuf<uint16_t> slab_w;    // bit-sliced dictionary: weight range per global slab
-    DBuf<uint32_t> wkey_a, wkey_b;  // scratch: (length << 7 | weight) sort keys
+    DBuf<uint32_t> wt;        // bit-sliced K2: group weights (fp_gweight) per sorted position
+    DBuf<uint2> slab_w;       // bit-sliced dictionary: group-weight box (min, max bytes) per global slab
+    DBuf<uint32_t> wkey_a, wkey_b;  // scratch: (length << 16 | group weights) sort keys
     DBuf<uint32_t> d_slab_start, d_count;
     DBuf<uint64_t> d_plane_base;
     // scratch (len_b = lengths in sorted order; kept for query collections)
@@ -300,8 +300,9 @@ struct Collection {
         size_t tmp = 0;
         const unsigned grid = (unsigned)cdiv(n, 256);
         if (mode == kSliceDict) {
-            // stable sort by (length, weight): inside a length bucket the words are
-            // ordered by fingerprint weight, so K2 warps see narrow weight ranges
+            // stable sort by (length, group weights): inside a length bucket the
+            // words are ordered by their group weights, so K2 warps see narrow
+            // group-weight boxes
             wkey_a.reserve(n);
             wkey_b.reserve(n);
 #define FPG_KEYS(V) fpg::k_weight_keys<V><<<grid, 256, 0, st>>>(d_blob, d_offs, n, P, wkey_a.p)
@@ -315,10 +316,10 @@ struct Collection {
             CK(cudaGetLastError());
             ++launches;
             CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, wkey_a.p, wkey_b.p, idx_a.p, idx_b.p, (int)n, 0,
-                                               end_bit + 7, st));
+                                               end_bit + 16, st));
             cub_tmp.reserve(tmp);
             CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, tmp, wkey_a.p, wkey_b.p, idx_a.p, idx_b.p, (int)n, 0,
-                                               end_bit + 7, st));
+                                               end_bit + 16, st));
             wt.reserve(n);
         } else {
             CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, len_a.p, len_b.p, idx_a.p, idx_b.p, (int)n, 0,
@@ -398,7 +399,7 @@ struct Collection {
         uint64_t* cmp_p = mode == kGenericDict ? cmp.p : nullptr;
         uint32_t* sig_p = mode == kGenericDict ? sig.p : nullptr;
         uint32_t* sigp_p = mode == kGenericDict ? nullptr : sigp.p;
-        uint8_t* wt_p = nullptr;
+        uint32_t* wt_p = nullptr;
         if (mode == kSliceQuery) {
             wt.reserve(n);
             wt_p = wt.p;

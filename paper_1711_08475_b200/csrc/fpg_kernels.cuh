@@ -141,28 +141,41 @@ __device__ __forceinline__ uint64_t onehot_count16(uint64_t fp) {
     return r;
 }
 
-// Fingerprint weight: the number of "present" fields (occurrence / halved:
-// set bits; count: non-zero counters; position: letters whose first position
-// is recorded, plus the extra occurrence bits).  One differing field changes
-// it by at most one, so |weight(a) - weight(b)| <= F_D (fingerprint.hpp:171-214):
-// K2 skips query / word groups whose weights differ by more than 2k.
-__device__ __forceinline__ uint32_t fp_weight(uint64_t fp, const SchemeParams& P) {
-    if (P.variant == 0 || P.variant == 1) return (uint32_t)__popcll(fp);
+// Group weights: the fields are dealt round robin into 4 groups (field i ->
+// group i & 3; occurrence / halved: bit i, count / position: the extra
+// one-bit fields, then the multi-bit fields), and byte g of the result is the
+// number of "present" fields of group g (occurrence / halved: set bits;
+// count: non-zero counters; position: letters whose first position is
+// recorded, plus the extra occurrence bits).  One differing field changes one
+// group's weight by at most one, so
+//   sum_g |gw_g(a) - gw_g(b)| <= F_D          (fingerprint.hpp:171-214)
+// and K2 skips query / word groups whose group-weight boxes are more than 2k
+// apart (L1 distance).
+__device__ __forceinline__ uint32_t fp_gweight(uint64_t fp, const SchemeParams& P) {
+    if (P.variant == 0 || P.variant == 1) {
+        uint32_t w = 0;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) w |= (uint32_t)__popcll(fp & (0x1111111111111111ull << g)) << (8 * g);
+        return w;
+    }
     const int fw = P.variant == 2 ? P.b : P.p;
     const int nf = P.variant == 2 ? P.width / P.b : P.slots;
     const int extra = P.variant == 2 ? 0 : P.extra;
     const uint64_t fmask = fw >= 64 ? ~0ull : ((1ull << fw) - 1);
-    const uint64_t emask = extra ? ((1ull << extra) - 1) : 0ull;  // position: extra one-bit fields
-    uint32_t w = (uint32_t)__popcll(fp & emask);
+    uint32_t w = 0;
+    for (int e = 0; e < extra; ++e) w += (uint32_t)((fp >> e) & 1u) << (8 * (e & 3));
     for (int f = 0; f < nf; ++f) {
         const uint64_t v = (fp >> (P.width - fw * (f + 1))) & fmask;
-        w += P.variant == 2 ? (v != 0) : (v != fmask);  // position: all-ones = absent
+        const bool present = P.variant == 2 ? (v != 0) : (v != fmask);  // position: all-ones = absent
+        w += (uint32_t)present << (8 * ((extra + f) & 3));
     }
     return w;
 }
 
-// Sort keys of the dictionary's K2 layout: (length << 7 | weight) per word in
-// input order (the fingerprint is computed here and again by k_build).
+// Sort keys of the dictionary's K2 layout: (length << 16 | group weights, 4
+// bits each, saturated at 15, group 0 most significant) per word in input
+// order (the fingerprint is computed here and again by k_build).  Saturation
+// only coarsens the order; K2's ranges use the exact group weights.
 template <int VARIANT>
 __global__ void __launch_bounds__(256) k_weight_keys(const uint8_t* __restrict__ blob,
                                                      const uint64_t* __restrict__ offsets, uint64_t n,
@@ -189,7 +202,11 @@ __global__ void __launch_bounds__(256) k_weight_keys(const uint8_t* __restrict__
                 if (q >= 0) fb.add(q, c + t, len, P);
             }
     }
-    keys[i] = ((uint32_t)len << 7) | fp_weight(fb.bits, P);
+    const uint32_t gw = fp_gweight(fb.bits, P);
+    uint32_t key = 0;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) key |= min((gw >> (8 * g)) & 0xffu, 15u) << (12 - 4 * g);
+    keys[i] = ((uint32_t)len << 16) | key;
 }
 
 // Inputs: raw blob + offsets, `order` = sorted position -> input index (stable
@@ -212,7 +229,7 @@ __global__ void __launch_bounds__(256) k_build(const uint8_t* __restrict__ blob,
                                                uint16_t* __restrict__ len_out = nullptr,
                                                uint32_t* __restrict__ zero_by_id = nullptr,
                                                unsigned long long* __restrict__ zero64 = nullptr,
-                                               int nzero64 = 0, uint8_t* __restrict__ weight_out = nullptr) {
+                                               int nzero64 = 0, uint32_t* __restrict__ weight_out = nullptr) {
     __shared__ int8_t s_slot[256];
     __shared__ int8_t s_sigbit[256];
     s_slot[threadIdx.x] = P.slot[threadIdx.x];           // blockDim == 256
@@ -255,7 +272,7 @@ __global__ void __launch_bounds__(256) k_build(const uint8_t* __restrict__ blob,
     if (sig_out) sig_out[pos] = sig;
     if (sigp_out) sigp_out[pos] = sigp;
     if (id_out) id_out[pos] = id;
-    if (weight_out) weight_out[pos] = (uint8_t)fp_weight(fp, P);
+    if (weight_out) weight_out[pos] = fp_gweight(fp, P);
 }
 
 // Lengths, identity ids and the length histogram (lengths < 256 counted in

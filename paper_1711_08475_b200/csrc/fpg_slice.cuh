@@ -25,9 +25,10 @@
 // 1.0-1.5 ALU ops per comparison for a 16-bit fingerprint, against the POPC
 // pipe's 16/clk/SM bound of a per-pair XOR + POPC.
 //
-// Weight window.  |weight(q) - weight(x)| <= F_D (fp_weight), so a warp skips
-// the queries whose weight is more than 2k away from its slabs' range: those
-// pairs are rejected by the reference test anyway.
+// Weight window.  sum_g |gw_g(q) - gw_g(x)| <= F_D over 4 field groups
+// (fp_gweight), so a warp skips the queries whose group weights are more than
+// 2k (L1) away from its slabs' group-weight box: those pairs are rejected by
+// the reference test anyway.
 //
 // sig' (internal, exact).  Bytes that are NOT scheme letters are dealt into S
 // extra one-bit occurrence fields (host LUT, frequency round robin).  One edit
@@ -99,8 +100,8 @@ struct SliceParams {
     int32_t stats;
     int32_t use_fp;             // scheme fields bound this metric (variant_supports, fingerprint.hpp:36-38)
     int32_t wskip;              // skip query / slab-group pairs whose weights differ by more than 2k
-    const uint8_t* q_weight;    // per sorted query: fingerprint weight (fp_weight)
-    const uint16_t* slab_w;     // per global slab: min | max << 8 of its words' weights
+    const uint32_t* q_weight;   // per sorted query: group weights (fp_gweight, one byte per group)
+    const uint2* slab_w;        // per global slab: per-byte min / max of its words' group weights
     unsigned long long* scanned;  // pairs actually evaluated (after the weight skip)
     int32_t exhaustive;         // verify every pair: no fingerprint / sig' pruning (naive-path timing)
 };
@@ -111,6 +112,20 @@ __device__ __forceinline__ int stride_of_len(int len) { return len <= 16 ? 16 : 
 __device__ __forceinline__ uint32_t qxor(uint32_t p, uint32_t s, uint32_t m) { return p * s + m; }
 // bitwise majority (the carry of a full adder): one LOP3
 __device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (c & (a | b)); }
+// Per-byte min of lo and max of hi over the warp: a group-weight box.
+__device__ __forceinline__ uint2 warp_box(uint32_t lo, uint32_t hi) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        lo = __vminu4(lo, __shfl_xor_sync(0xffffffffu, lo, d));
+        hi = __vmaxu4(hi, __shfl_xor_sync(0xffffffffu, hi, d));
+    }
+    return make_uint2(lo, hi);
+}
+// L1 distance between a query's group weights and a box: at most one of the
+// two saturated differences of a byte is non-zero.
+__device__ __forceinline__ uint32_t box_dist(uint32_t q, uint2 box) {
+    return __vsadu4(__vsubus4(box.x, q) | __vsubus4(q, box.y), 0u);
+}
 
 template <int NP, int FW, int EXTRA, int S>
 struct SliceShape {
@@ -142,7 +157,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
     uint16_t* s_qlist = reinterpret_cast<uint16_t*>(s_wbuf + kSliceWarpBuf * kSliceWarps);  // [warps][kSliceQ]
     __shared__ uint32_t s_next[2];  // next tile index, double-buffered by iteration parity
     __shared__ uint32_t s_surv[kSliceQ];
-    __shared__ uint8_t s_qw[kSliceQ];  // query weights
+    __shared__ uint32_t s_qw[kSliceQ];  // query group weights
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     unsigned long long surv_warp = 0;  // lane 0: the warp's fingerprint survivors
     uint32_t cand_lane = 0;
@@ -178,7 +193,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
             s_qinfo[j] = (uint32_t)m;
             s_qid[j] = id;
             s_surv[j] = 0u;
-            s_qw[j] = P.wskip ? P.q_weight[qp] : 0;
+            s_qw[j] = P.wskip ? P.q_weight[qp] : 0u;
         }
         // this lane's slabs: warp w owns the 32 SL consecutive slabs from
         // tl.slab_begin + 32 SL w (weights are sorted inside a length bucket,
@@ -186,7 +201,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
         // 32 r + l of them
         uint32_t pl[SL][NPT];
         uint32_t valid[SL];
-        uint32_t wlo = 0xffu, whi = 0u;  // this lane's slabs' weight range
+        uint32_t wlo = 0xffffffffu, whi = 0u;  // this lane's slabs' group-weight box (per byte)
 #pragma unroll
         for (int r = 0; r < SL; ++r) {
             const uint32_t rel = 32u * SL * warp + 32u * r + (uint32_t)lane;
@@ -198,9 +213,9 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
             const uint32_t rem = tl.w_count - 32u * slab;  // words left in the bucket from this slab on
             valid[r] = !ok ? 0u : rem >= 32u ? 0xffffffffu : ((1u << rem) - 1u);
             if (ok && P.wskip) {
-                const uint32_t mm = __ldg(P.slab_w + tl.slab_g0 + slab);
-                wlo = min(wlo, mm & 0xffu);
-                whi = max(whi, mm >> 8);
+                const uint2 mm = __ldg(P.slab_w + tl.slab_g0 + slab);
+                wlo = __vminu4(wlo, mm.x);
+                whi = __vmaxu4(whi, mm.y);
             }
         }
         __syncthreads();
@@ -407,20 +422,20 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
 #undef FPG_QS
 #undef FPG_QM
         };
-        // This warp's queries: those whose weight is within 2k of its slabs'
-        // weight range (the others have F_D > 2k with every word here:
-        // |weight difference| <= F_D), compacted into a list.
+        // This warp's queries: those whose group weights are within L1
+        // distance 2k of its slabs' group-weight box (the others have F_D > 2k
+        // with every word here: sum_g |group weight difference| <= F_D),
+        // compacted into a list.
         uint32_t nlist = 0;
         {
-            const uint32_t lo = __reduce_min_sync(0xffffffffu, wlo), hi = __reduce_max_sync(0xffffffffu, whi);
+            const uint2 box = warp_box(wlo, whi);
             const uint32_t span = 2u * (uint32_t)P.k;
             uint16_t* ql = s_qlist + warp * kSliceQ;
             for (uint32_t b = 0; b < tl.q_count; b += 32) {
                 const uint32_t j = b + (uint32_t)lane;
-                bool in = j < tl.q_count;
+                bool in = j < tl.q_count && 32u * SL * warp < tl.n_slabs;
                 if (in && P.wskip) {
-                    const uint32_t w = s_qw[j];
-                    in = w + span >= lo && w <= hi + span;
+                    in = box_dist(s_qw[j], box) <= span;
                 }
                 const uint32_t bal = __ballot_sync(0xffffffffu, in);
                 if (in) ql[nlist + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)j;
@@ -461,7 +476,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
 // One warp per slab: lane i holds word 32 s + i of its bucket; plane b is the
 // ballot of bit b of the words' codes (fingerprint bits, then sig' bits).
 __global__ void k_planes(const uint64_t* __restrict__ fp, const uint32_t* __restrict__ sigp,
-                         const uint8_t* __restrict__ weight, uint16_t* __restrict__ slab_w,
+                         const uint32_t* __restrict__ weight, uint2* __restrict__ slab_w,
                          const uint32_t* __restrict__ slab_start,  // per length: first global slab (L1 + 1)
                          const uint32_t* __restrict__ start,       // per length: first sorted position
                          const uint32_t* __restrict__ count,       // per length: words
@@ -483,11 +498,10 @@ __global__ void k_planes(const uint64_t* __restrict__ fp, const uint32_t* __rest
     const bool ok = w < count[L];
     const uint64_t f = ok ? fp[start[L] + w] : 0ull;
     const uint32_t g = ok ? sigp[start[L] + w] : 0u;
-    if (slab_w) {  // the slab's weight range (K2's weight window)
+    if (slab_w) {  // the slab's group-weight box (K2's weight window): per-byte min / max
         const uint32_t wt = ok ? weight[start[L] + w] : 0u;
-        const uint32_t lo = __reduce_min_sync(0xffffffffu, ok ? wt : 0xffu);
-        const uint32_t hi = __reduce_max_sync(0xffffffffu, ok ? wt : 0u);
-        if (lane == 0) slab_w[gs] = (uint16_t)(lo | (hi << 8));
+        const uint2 box = warp_box(ok ? wt : 0xffffffffu, ok ? wt : 0u);
+        if (lane == 0) slab_w[gs] = box;
     }
     uint32_t mine[3] = {0u, 0u, 0u};
 #pragma unroll

@@ -60,6 +60,16 @@ def report(path, nlines=25):
     for k in RAW_KEYS:
         if k in d:
             print(f"  {k} = {d[k]} {u.get(k, '')}")
+    st = []
+    for k, v in d.items():
+        if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
+            try:
+                st.append((float(v.replace(",", "")), k[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
+            except ValueError:
+                pass
+    if st:
+        print("  stall reasons (warps per issue-active cycle): " +
+              ", ".join(f"{n} {x:.2f}" for x, n in sorted(st, reverse=True)[:8]))
     src = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout
     out, fname = [], None
