@@ -40,7 +40,8 @@ def build_fpg(force: bool = False) -> Path:
     srcs = sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "fpg.h"]
     if force or _stale(out, srcs):
         tmp = out.with_suffix(".so.tmp")
-        cmd = [_nvcc(), *NVCC_FLAGS, "-o", str(tmp), str(CSRC / "fpg_api.cu")]
+        dbg = ["-DFPG_DEBUG"] if os.environ.get("FPG_DEBUG") == "1" else []
+        cmd = [_nvcc(), *NVCC_FLAGS, *dbg, "-o", str(tmp), str(CSRC / "fpg_api.cu")]
         subprocess.run(cmd, check=True)
         os.replace(tmp, out)
     return out

@@ -693,14 +693,17 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         // Tile plan: per word length lw, the compatible query lengths form one
         // contiguous range of the length-sorted queries (Hamming / k = 0:
         // lw; Levenshtein k = 1: lw - 1 .. lw + 1, edit_distance.hpp:38-39).
-        // Tiles = (<= 256 SL slabs) x (<= kSliceQ queries), largest first,
+        // Tiles = (<= kSliceMaxSlabs slabs) x (<= kSliceQ queries), largest first,
         // handed out by an atomic counter.
         const int L1 = fpg::kMaxLen + 1;
-        // Tile shape: 128 queries x 256 SL slabs, made smaller (queries down to
-        // 16, then slabs down to one warp's 32 SL) while a small batch would give
-        // fewer than ~4 tiles per resident CTA.
-        const uint32_t sl = (uint32_t)fpg::slice_slabs_per_lane(D->npt);
-        uint32_t per = fpg::kSliceThreads * sl, qchunk = fpg::kSliceQ;
+        // Tile shape: 128 queries x 32 slab groups (the warps claim the tile's
+        // groups dynamically, so one tile's query masks serve many groups),
+        // made smaller (slabs down to two groups per warp, queries down to 32,
+        // slabs down to one group per warp, queries down to 16, then slabs down
+        // to one group) while the batch would give fewer than ~4 tiles per
+        // resident CTA.
+        const uint32_t grp = (uint32_t)fpg::slice_group_slabs(D->npt);
+        uint32_t per = 32 * grp, qchunk = fpg::kSliceQ;
         {
             int sms = 148;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, sh.device);
@@ -715,8 +718,12 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
                 }
                 return c;
             };
-            while (count_tiles() < target && (qchunk > 16 || per > 32u * sl)) {
-                if (qchunk > 16) qchunk >>= 1;
+            const uint32_t w8 = (uint32_t)fpg::kSliceWarps * grp;
+            while (count_tiles() < target && (qchunk > 16 || per > grp)) {
+                if (per > 2 * w8) per >>= 1;                   // down to 2 groups per warp
+                else if (qchunk > 32) qchunk >>= 1;            // then 32 queries
+                else if (per > w8) per >>= 1;                  // then 1 group per warp
+                else if (qchunk > 16) qchunk >>= 1;
                 else per >>= 1;
             }
         }

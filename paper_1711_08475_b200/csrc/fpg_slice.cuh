@@ -52,6 +52,20 @@
 
 namespace fpg {
 
+// Device-side bounds checks for debug builds (FPG_DEBUG=1 python build.py).
+#ifdef FPG_DEBUG
+#define FPG_CHECK(c)                                                                           \
+    do {                                                                                       \
+        if (!(c)) {                                                                            \
+            printf("FPG_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                         \
+            __trap();                                                                          \
+        }                                                                                      \
+    } while (0)
+#else
+#define FPG_CHECK(c) do { } while (0)
+#endif
+
 constexpr int kSliceThreads = 256;
 constexpr int kSliceWarps = kSliceThreads / 32;
 constexpr int kSliceQ = 128;      // queries per tile (shared-memory masks)
@@ -59,6 +73,8 @@ constexpr int kSliceCap = 8;      // queue entries per lane
 constexpr int kSliceWarpBuf = 256;  // expanded candidates per warp and verify round
 
 __host__ __device__ constexpr int slice_slabs_per_lane(int npt) { return npt <= 40 ? 2 : 1; }
+// Slabs per slab group: the unit a warp claims inside a tile (32 per lane row).
+__host__ __device__ constexpr int slice_group_slabs(int npt) { return 32 * slice_slabs_per_lane(npt); }
 
 struct SliceTile {
     uint32_t slab_begin;   // first slab of the tile, bucket-local
@@ -155,6 +171,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
     uint2* s_queue = reinterpret_cast<uint2*>(s_qid + kSliceQ);             // [cap][threads]
     uint32_t* s_wbuf = reinterpret_cast<uint32_t*>(s_queue + kSliceCap * kSliceThreads);  // [warps][buf]
     uint16_t* s_qlist = reinterpret_cast<uint16_t*>(s_wbuf + kSliceWarpBuf * kSliceWarps);  // [warps][kSliceQ]
+    __shared__ uint32_t s_grp;  // next slab group of the tile
     __shared__ uint32_t s_next[2];  // next tile index, double-buffered by iteration parity
     __shared__ uint32_t s_surv[kSliceQ];
     __shared__ uint32_t s_qw[kSliceQ];  // query group weights
@@ -195,29 +212,40 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
             s_surv[j] = 0u;
             s_qw[j] = P.wskip ? P.q_weight[qp] : 0u;
         }
-        // this lane's slabs: warp w owns the 32 SL consecutive slabs from
-        // tl.slab_begin + 32 SL w (weights are sorted inside a length bucket,
-        // so a warp's slabs span a narrow weight range); lane l takes slab
-        // 32 r + l of them
+        // this lane's slabs of slab group g (SL rows of 32 slabs), the
+        // group's valid words and its group-weight box
         uint32_t pl[SL][NPT];
         uint32_t valid[SL];
-        uint32_t wlo = 0xffffffffu, whi = 0u;  // this lane's slabs' group-weight box (per byte)
+        uint32_t vw = 0;
+        uint2 box = make_uint2(0u, 0u);
+        const uint32_t n_grp = (tl.n_slabs + 32u * SL - 1u) / (32u * SL);
+        auto load_group = [&](uint32_t g) {
+            uint32_t wlo = 0xffffffffu, whi = 0u;
+            vw = 0;
 #pragma unroll
-        for (int r = 0; r < SL; ++r) {
-            const uint32_t rel = 32u * SL * warp + 32u * r + (uint32_t)lane;
-            const uint32_t slab = tl.slab_begin + rel;
-            const bool ok = rel < tl.n_slabs;
-            const uint32_t* src = P.planes + tl.plane_base + slab;
+            for (int r = 0; r < SL; ++r) {
+                const uint32_t rel = 32u * (SL * g + r) + (uint32_t)lane;
+                const uint32_t slab = tl.slab_begin + rel;
+                const bool ok = rel < tl.n_slabs;
+                const uint32_t* src = P.planes + tl.plane_base + slab;
 #pragma unroll
-            for (int b = 0; b < NPT; ++b) pl[r][b] = ok ? __ldg(src + (size_t)b * tl.ns) : 0u;
-            const uint32_t rem = tl.w_count - 32u * slab;  // words left in the bucket from this slab on
-            valid[r] = !ok ? 0u : rem >= 32u ? 0xffffffffu : ((1u << rem) - 1u);
-            if (ok && P.wskip) {
-                const uint2 mm = __ldg(P.slab_w + tl.slab_g0 + slab);
-                wlo = __vminu4(wlo, mm.x);
-                whi = __vmaxu4(whi, mm.y);
+                for (int b = 0; b < NPT; ++b) pl[r][b] = ok ? __ldg(src + (size_t)b * tl.ns) : 0u;
+                const uint32_t rem = tl.w_count - 32u * slab;  // words left in the bucket from this slab on
+                valid[r] = !ok ? 0u : rem >= 32u ? 0xffffffffu : ((1u << rem) - 1u);
+                vw += __popc(valid[r]);
+                if (ok && P.wskip) {
+                    const uint2 mm = __ldg(P.slab_w + tl.slab_g0 + slab);
+                    wlo = __vminu4(wlo, mm.x);
+                    whi = __vmaxu4(whi, mm.y);
+                }
             }
-        }
+            box = make_uint2(wlo, whi);
+        };
+        // warp w's first group is group w: its planes load while the queries
+        // are set up; later groups are claimed from s_grp
+        uint32_t g = (uint32_t)warp;
+        if (g < n_grp) load_group(g);
+        if (tid == 0) s_grp = (uint32_t)kSliceWarps;
         __syncthreads();
 
         uint32_t qn = 0;  // queued entries of this lane
@@ -246,12 +274,18 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 uint32_t rank = incl - c;
                 for (uint32_t s = 0; s < qn && rank < (uint32_t)kSliceWarpBuf; ++s) {
                     uint2 e = s_queue[s * kSliceThreads + tid];
-                    const uint32_t j = e.x & 0xffffu, r = e.x >> 16;
-                    const uint32_t wt0 = 32u * (32u * SL * warp + 32u * r + (uint32_t)lane);  // word index within the tile
+                    const uint32_t j = e.x & 0xffffu, row = e.x >> 16;  // tile query, tile slab row
+#ifdef FPG_DEBUG
+                    if (!(j < tl.q_count && 32u * row < tl.n_slabs))
+                        printf("bad entry: j %u q_count %u row %u n_slabs %u y %x s %u qn %u tile %u\n", j, tl.q_count, row,
+                               tl.n_slabs, e.y, s, qn, t);
+#endif
+                    FPG_CHECK(j < tl.q_count && 32u * row < tl.n_slabs);
+                    const uint32_t wt0 = 32u * (32u * row + (uint32_t)lane);  // word index within the tile
                     while (e.y && rank < (uint32_t)kSliceWarpBuf) {
                         const int i = __ffs(e.y) - 1;
                         e.y &= e.y - 1;
-                        wbuf[rank++] = (j << 16) | (wt0 + (uint32_t)i);
+                        wbuf[rank++] = (j << 25) | (wt0 + (uint32_t)i);
                     }
                     s_queue[s * kSliceThreads + tid].y = e.y;
                 }
@@ -264,8 +298,14 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                     uint32_t j = 0, widx = 0;
                     if (idx < m_all) {
                         const uint32_t v = wbuf[idx];
-                        j = v >> 16;
-                        widx = 32u * tl.slab_begin + (v & 0xffffu);
+                        j = v >> 25;
+                        widx = 32u * tl.slab_begin + (v & 0x1ffffffu);
+#ifdef FPG_DEBUG
+                        if (!(j < tl.q_count && widx < tl.w_count))
+                            printf("bad cand: j %u q_count %u widx %u w_count %u v %x slab_begin %u n_slabs %u idx %u m_all %u total %u\n",
+                                   j, tl.q_count, widx, tl.w_count, v, tl.slab_begin, tl.n_slabs, idx, m_all, total);
+#endif
+                        FPG_CHECK(j < tl.q_count && widx < tl.w_count);
                         const int m = (int)s_qinfo[j], n = tl.w_len;
                         const int ws = tl.w_stride;
                         const uint8_t* wb = P.w_bytes + tl.w_bytes + (uint64_t)widx * ws;
@@ -312,6 +352,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
         // lane's SLX slabs: NQ * SLX independent counter chains per plane.
         // step over list entries i .. i + NQ - 1 (tile query indices)
         const uint16_t* qlist = s_qlist + warp * kSliceQ;
+        uint32_t row0 = 0;  // tile slab row of this lane's pl[0]
         auto step = [&](auto slc, auto nqc, uint32_t i) {
             constexpr int SLX = decltype(slc)::value;
             constexpr int NQ = decltype(nqc)::value;
@@ -413,50 +454,61 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                     for (int r = 0; r < SLX; ++r) {
                         const uint32_t cand = P.exhaustive ? valid[r] : valid[r] & ~rejected(h, r);
                         if (cand) {
-                            s_queue[qn * kSliceThreads + tid] = make_uint2(jq[h] | ((uint32_t)r << 16), cand);
+                            s_queue[qn * kSliceThreads + tid] = make_uint2(jq[h] | ((row0 + (uint32_t)r) << 16), cand);
                             ++qn;
                         }
                     }
-                if (__any_sync(0xffffffffu, qn > (uint32_t)(kSliceCap - NQ * SLX))) flush();
+                // room for the largest step (2 queries x SL slabs) whatever comes next
+                if (__any_sync(0xffffffffu, qn > (uint32_t)(kSliceCap - 2 * SL))) flush();
             }
 #undef FPG_QS
 #undef FPG_QM
         };
-        // This warp's queries: those whose group weights are within L1
-        // distance 2k of its slabs' group-weight box (the others have F_D > 2k
-        // with every word here: sum_g |group weight difference| <= F_D),
-        // compacted into a list.
-        uint32_t nlist = 0;
+        // Slab groups (SL rows of 32 slabs) are claimed one at a time from
+        // s_grp: no barrier between them, so the warps of a tile stay busy
+        // whatever the weight window leaves per group, and the tile's query
+        // masks serve all of its groups.  Per group: the lane's slab planes
+        // into registers, the group's weight box, and the list of tile queries
+        // whose group weights are within L1 distance 2k of the box (the others
+        // have F_D > 2k with every word of the group: sum_g |group weight
+        // difference| <= F_D).
         {
-            const uint2 box = warp_box(wlo, whi);
             const uint32_t span = 2u * (uint32_t)P.k;
             uint16_t* ql = s_qlist + warp * kSliceQ;
-            for (uint32_t b = 0; b < tl.q_count; b += 32) {
-                const uint32_t j = b + (uint32_t)lane;
-                bool in = j < tl.q_count && 32u * SL * warp < tl.n_slabs;
-                if (in && P.wskip) {
-                    in = box_dist(s_qw[j], box) <= span;
+            for (bool first = true;; first = false) {
+                if (!first) {
+                    if (lane == 0) g = atomicAdd(&s_grp, 1u);
+                    g = __shfl_sync(0xffffffffu, g, 0);
+                    if (g < n_grp) load_group(g);
                 }
-                const uint32_t bal = __ballot_sync(0xffffffffu, in);
-                if (in) ql[nlist + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)j;
-                nlist += __popc(bal);
+                if (g >= n_grp) break;
+                row0 = (uint32_t)SL * g;
+                box = warp_box(box.x, box.y);
+                uint32_t nlist = 0;
+                for (uint32_t b = 0; b < tl.q_count; b += 32) {
+                    const uint32_t j = b + (uint32_t)lane;
+                    bool in = j < tl.q_count;
+                    if (in && P.wskip) in = box_dist(s_qw[j], box) <= span;
+                    const uint32_t bal = __ballot_sync(0xffffffffu, in);
+                    if (in) ql[nlist + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)j;
+                    nlist += __popc(bal);
+                }
+                __syncwarp();
+                // pairs actually evaluated (stats / roofline)
+                const uint32_t vws = __reduce_add_sync(0xffffffffu, vw);
+                if (lane == 0 && verify) scanned_warp += (unsigned long long)vws * nlist;
+                uint32_t i = 0;
+                if (SL == 2 && 32u * (row0 + 1u) < tl.n_slabs) {
+                    if constexpr (NPT <= 48)  // query pairs while the registers allow it
+                        for (; i + 2 <= nlist; i += 2) step(std::integral_constant<int, SL>{}, std::integral_constant<int, 2>{}, i);
+                    for (; i < nlist; ++i) step(std::integral_constant<int, SL>{}, std::integral_constant<int, 1>{}, i);
+                } else {
+                    if constexpr (NPT <= 48)
+                        for (; i + 2 <= nlist; i += 2) step(std::integral_constant<int, 1>{}, std::integral_constant<int, 2>{}, i);
+                    for (; i < nlist; ++i) step(std::integral_constant<int, 1>{}, std::integral_constant<int, 1>{}, i);
+                }
             }
-            __syncwarp();
-            // pairs actually evaluated by this warp (stats / roofline)
-            uint32_t vw = 0;
-#pragma unroll
-            for (int r = 0; r < SL; ++r) vw += __popc(valid[r]);
-            vw = __reduce_add_sync(0xffffffffu, vw);
-            if (lane == 0 && verify) scanned_warp += (unsigned long long)vw * nlist;
         }
-        auto scan_queries = [&](auto slc) {
-            uint32_t i = 0;
-            if constexpr (NPT <= 48)  // query pairs while the registers allow it
-                for (; i + 2 <= nlist; i += 2) step(slc, std::integral_constant<int, 2>{}, i);
-            for (; i < nlist; ++i) step(slc, std::integral_constant<int, 1>{}, i);
-        };
-        if (SL == 2 && 32u * SL * warp + 32u < tl.n_slabs) scan_queries(std::integral_constant<int, SL>{});
-        else scan_queries(std::integral_constant<int, 1>{});
         if (verify) flush();
         __syncthreads();  // tile consumed; s_next[it & 1] and s_surv complete
         if (P.stats)
