@@ -719,9 +719,13 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
                 return c;
             };
             const uint32_t w8 = (uint32_t)fpg::kSliceWarps * grp;
+            // FPG_TILE_GPW / FPG_TILE_Q: groups per warp and queries kept by the
+            // first two shrink stages (A/B runs)
+            static const uint32_t gpw = (uint32_t)env_double("FPG_TILE_GPW", 2.0);
+            static const uint32_t q1 = (uint32_t)env_double("FPG_TILE_Q", 32.0);
             while (count_tiles() < target && (qchunk > 16 || per > grp)) {
-                if (per > 2 * w8) per >>= 1;                   // down to 2 groups per warp
-                else if (qchunk > 32) qchunk >>= 1;            // then 32 queries
+                if (per > gpw * w8) per >>= 1;                 // down to gpw groups per warp
+                else if (qchunk > q1) qchunk >>= 1;            // then q1 queries
                 else if (per > w8) per >>= 1;                  // then 1 group per warp
                 else if (qchunk > 16) qchunk >>= 1;
                 else per >>= 1;
@@ -919,7 +923,8 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
             CK(cub::DeviceScan::ExclusiveSum(S.cub_tmp.p, tmp, S.qsurv.p + nq, S.offsets.p, (int)nq, st));
         }
         fpg::k_seg_scatter<<<kScatterBlocks, 256, 0, st>>>(S.out.p, S.counters.p, S.counters.p + 5, S.out.cap,
-                                                           S.offsets.p, S.qsurv.p + nq, S.ids.p, S.offsets.p + nq);
+                                                           S.offsets.p, S.qsurv.p + nq, S.ids.p, S.offsets.p + nq,
+                                                           W.ids.p, D->id_base + sh.base);
         CK(cudaGetLastError());
         S.launches += 2;
         if (warp_sort) {

@@ -371,7 +371,8 @@ __device__ __forceinline__ bool match_run_head(bool hit, uint32_t qid, uint32_t 
 __global__ void k_seg_scatter(const unsigned long long* __restrict__ keys, const unsigned long long* __restrict__ slots,
                               const unsigned long long* __restrict__ matches, uint64_t cap,
                               const uint64_t* __restrict__ offsets_in, uint32_t* __restrict__ cursor,
-                              uint32_t* __restrict__ ids, uint64_t* __restrict__ offsets_last) {
+                              uint32_t* __restrict__ ids, uint64_t* __restrict__ offsets_last,
+                              const uint32_t* __restrict__ w_ids, uint64_t id_base) {
     const uint64_t used = *slots;
     const uint64_t n = used < cap ? used : cap;  // overflowed runs are redone by the host
     const uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -392,7 +393,9 @@ __global__ void k_seg_scatter(const unsigned long long* __restrict__ keys, const
         if (lane == leader) base = atomicSub(&cursor[q], cnt) - cnt;
         base = __shfl_sync(peers, base, leader);
         const uint64_t pos = offsets_in[q] + base + (uint32_t)__popc(peers & ((1u << lane) - 1u));
-        if (pos < cap) ids[pos] = (uint32_t)k;
+        // K2 keys carry the word's sorted position: map it to the input-order
+        // id here, where the gathers of a whole warp are in flight at once
+        if (pos < cap) ids[pos] = (uint32_t)(id_base + __ldg(w_ids + (uint32_t)k));
     }
 }
 

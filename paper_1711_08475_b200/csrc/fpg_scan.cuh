@@ -333,7 +333,7 @@ struct TileScan {
                     const uint32_t qid = hit ? P.q_ids[tl.q_begin + j] : 0xffffffffu;
                     const bool head = match_run_head(hit, qid, hb);
                     const uint32_t heads = __ballot_sync(0xffffffffu, head);
-                    const uint64_t wid = hit ? P.id_base + P.w_ids[tl.w_begin + widx] : 0;
+                    const uint64_t wid = hit ? (uint64_t)(tl.w_begin + widx) : 0;  // sorted position (K4 maps it)
                     oc.emit(hb, hit, ((uint64_t)qid << 32) | wid, P.out, P.out_cap, P.out_count);
                     if (hit) count_match(P.q_matches, qid, hb, head, heads);
                 }

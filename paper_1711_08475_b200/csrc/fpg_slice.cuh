@@ -292,52 +292,64 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 __syncwarp();
                 const uint32_t m_all = min(total, (uint32_t)kSliceWarpBuf);
                 cand_lane += (lane == 0) ? m_all : 0u;
-                for (uint32_t base = 0; base < m_all; base += 32) {
-                    const uint32_t idx = base + lane;
-                    bool hit = false;
-                    uint32_t j = 0, widx = 0;
-                    if (idx < m_all) {
-                        const uint32_t v = wbuf[idx];
-                        j = v >> 25;
-                        widx = 32u * tl.slab_begin + (v & 0x1ffffffu);
-#ifdef FPG_DEBUG
-                        if (!(j < tl.q_count && widx < tl.w_count))
-                            printf("bad cand: j %u q_count %u widx %u w_count %u v %x slab_begin %u n_slabs %u idx %u m_all %u total %u\n",
-                                   j, tl.q_count, widx, tl.w_count, v, tl.slab_begin, tl.n_slabs, idx, m_all, total);
-#endif
-                        FPG_CHECK(j < tl.q_count && widx < tl.w_count);
-                        const int m = (int)s_qinfo[j], n = tl.w_len;
-                        const int ws = tl.w_stride;
-                        const uint8_t* wb = P.w_bytes + tl.w_bytes + (uint64_t)widx * ws;
-                        const int mx = m > n ? m : n;
-                        if (mx <= 16) {
-                            uint32_t a[4], bb[4];
-                            const uint4 qa = s_qb[2 * j];
-                            a[0] = qa.x; a[1] = qa.y; a[2] = qa.z; a[3] = qa.w;
-                            load_padded<4>(wb, ws, bb);
-                            hit = verify_regs<4>(a, bb, m, n, P.k);
-                        } else if (mx <= 32) {
-                            uint32_t a[8], bb[8];
-                            const uint4 qa = s_qb[2 * j], qc = s_qb[2 * j + 1];
-                            a[0] = qa.x; a[1] = qa.y; a[2] = qa.z; a[3] = qa.w;
-                            a[4] = qc.x; a[5] = qc.y; a[6] = qc.z; a[7] = qc.w;
-                            load_padded<8>(wb, ws, bb);
-                            hit = verify_regs<8>(a, bb, m, n, P.k);
-                        } else {
-                            const uint32_t qpos = tl.q_begin + j;
-                            const int qs = stride_of_len(m);
-                            const uint8_t* qb = P.q_bytes + P.q_bbase[m] + (uint64_t)(qpos - P.q_start[m]) * qs;
-                            hit = verify_pair(qb, m, qs, wb, n, ws, P.k);
+                // two candidates per lane per round: both words' bytes are
+                // requested before either is compared (memory-level parallelism)
+                for (uint32_t base = 0; base < m_all; base += 64) {
+                    uint32_t jj[2], wi[2], bw[2][8];
+                    int mm[2];
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const uint32_t idx = base + 32u * u + lane;
+                        jj[u] = 0; wi[u] = 0; mm[u] = -1;
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) bw[u][c] = 0u;
+                        if (idx < m_all) {
+                            const uint32_t v = wbuf[idx];
+                            jj[u] = v >> 25;
+                            wi[u] = 32u * tl.slab_begin + (v & 0x1ffffffu);
+                            FPG_CHECK(jj[u] < tl.q_count && wi[u] < tl.w_count);
+                            mm[u] = (int)s_qinfo[jj[u]];
+                            const int mx = mm[u] > tl.w_len ? mm[u] : tl.w_len;
+                            if (mx <= 32) load_padded<8>(P.w_bytes + tl.w_bytes + (uint64_t)wi[u] * tl.w_stride, tl.w_stride, bw[u]);
                         }
                     }
-                    const uint32_t hb = __ballot_sync(0xffffffffu, hit);
-                    if (hb) {
-                        const uint32_t qid = s_qid[j];
-                        const bool head = match_run_head(hit, qid, hb);
-                        const uint32_t heads = __ballot_sync(0xffffffffu, head);
-                        const uint64_t wid = hit ? P.id_base + P.w_ids[tl.w_start + widx] : 0;
-                        oc.emit(hb, hit, ((uint64_t)qid << 32) | wid, P.out, P.out_cap, P.out_count);
-                        if (hit) count_match(P.q_matches, qid, hb, head, heads);
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        bool hit = false;
+                        const uint32_t j = jj[u], widx = wi[u];
+                        if (mm[u] >= 0) {
+                            const int m = mm[u], n = tl.w_len;
+                            const int mx = m > n ? m : n;
+                            if (mx <= 16) {
+                                uint32_t a4[4], b4[4];
+                                const uint4 qa = s_qb[2 * j];
+                                a4[0] = qa.x; a4[1] = qa.y; a4[2] = qa.z; a4[3] = qa.w;
+                                b4[0] = bw[u][0]; b4[1] = bw[u][1]; b4[2] = bw[u][2]; b4[3] = bw[u][3];
+                                hit = verify_regs<4>(a4, b4, m, n, P.k);
+                            } else if (mx <= 32) {
+                                uint32_t a8[8];
+                                const uint4 qa = s_qb[2 * j], qc = s_qb[2 * j + 1];
+                                a8[0] = qa.x; a8[1] = qa.y; a8[2] = qa.z; a8[3] = qa.w;
+                                a8[4] = qc.x; a8[5] = qc.y; a8[6] = qc.z; a8[7] = qc.w;
+                                hit = verify_regs<8>(a8, bw[u], m, n, P.k);
+                            } else {
+                                const uint32_t qpos = tl.q_begin + j;
+                                const int qs = stride_of_len(m);
+                                const uint8_t* qb = P.q_bytes + P.q_bbase[m] + (uint64_t)(qpos - P.q_start[m]) * qs;
+                                const uint8_t* wb = P.w_bytes + tl.w_bytes + (uint64_t)widx * tl.w_stride;
+                                hit = verify_pair(qb, m, qs, wb, n, tl.w_stride, P.k);
+                            }
+                        }
+                        const uint32_t hb = __ballot_sync(0xffffffffu, hit);
+                        if (hb) {
+                            const uint32_t qid = s_qid[j];
+                            const bool head = match_run_head(hit, qid, hb);
+                            const uint32_t heads = __ballot_sync(0xffffffffu, head);
+                            // sorted position; K4 maps it to the input-order id
+                            const uint64_t wid = hit ? (uint64_t)(tl.w_start + widx) : 0;
+                            oc.emit(hb, hit, ((uint64_t)qid << 32) | wid, P.out, P.out_cap, P.out_count);
+                            if (hit) count_match(P.q_matches, qid, hb, head, heads);
+                        }
                     }
                 }
                 __syncwarp();
