@@ -995,7 +995,9 @@ void check_opts(const fpg_dict* D, const fpg_query_options* o) {
                                           std::to_string(o->k));
 }
 
-void upload(fpg_batch* B, const uint8_t* qbytes, const uint64_t* qoffsets, uint64_t nq) {
+// sync = false (fpg_query_batch): the caller's buffers stay valid until the
+// call returns, so the copies may still be in flight when upload returns.
+void upload(fpg_batch* B, const uint8_t* qbytes, const uint64_t* qoffsets, uint64_t nq, bool sync = true) {
     const auto t0 = std::chrono::steady_clock::now();
     if (nq && !qoffsets) throw Error(FPG_EINVAL, "null query offsets");
     if (nq >= (1ull << 31)) throw Error(FPG_EINVAL, "too many queries in one batch");
@@ -1004,13 +1006,18 @@ void upload(fpg_batch* B, const uint8_t* qbytes, const uint64_t* qoffsets, uint6
     const int L1 = fpg::kMaxLen + 1;
     B->qcount.assign(L1, 0);
     const uint64_t q0 = nq ? qoffsets[0] : 0;
+    uint64_t len_max = 0;
     for (uint64_t i = 0; i < nq; ++i) {
-        if (qoffsets[i + 1] < qoffsets[i]) throw Error(FPG_EINVAL, "query offsets not ascending");
-        const uint64_t len = qoffsets[i + 1] - qoffsets[i];
-        if (len > (uint64_t)fpg::kMaxLen) throw Error(FPG_EINVAL, "query longer than FPG_MAX_WORD_LEN");
+        const uint64_t len = qoffsets[i + 1] - qoffsets[i];  // wraps (huge) if not ascending
+        len_max = len > len_max ? len : len_max;
         B->qlen[i] = (uint32_t)len;
-        ++B->qcount[len];
     }
+    if (len_max > (uint64_t)fpg::kMaxLen) {
+        for (uint64_t i = 0; i < nq; ++i)
+            if (qoffsets[i + 1] < qoffsets[i]) throw Error(FPG_EINVAL, "query offsets not ascending");
+        throw Error(FPG_EINVAL, "query longer than FPG_MAX_WORD_LEN");
+    }
+    for (uint64_t i = 0; i < nq; ++i) ++B->qcount[B->qlen[i]];
     if (nq && qoffsets[nq] > q0 && !qbytes) throw Error(FPG_EINVAL, "null query bytes");
     // Length buckets: stable counting sort of the query ids (the layout K1
     // writes, with the padded-byte offset of every bucket).
@@ -1021,7 +1028,7 @@ void upload(fpg_batch* B, const uint8_t* qbytes, const uint64_t* qoffsets, uint6
     B->h_order.reserve(nq);
     uint64_t pos = 0, bpos = 0;
     B->qmax_len = 0;
-    for (int L = 0; L < L1; ++L) {
+    for (int L = 0; L <= (int)len_max; ++L) {
         B->qstart[L] = (uint32_t)pos;
         B->qbbase[L] = bpos;
         B->h_start.p[L] = (uint32_t)pos;
@@ -1030,6 +1037,11 @@ void upload(fpg_batch* B, const uint8_t* qbytes, const uint64_t* qoffsets, uint6
         bpos += (uint64_t)B->qcount[L] * stride_of(L);
         if (B->qcount[L]) B->qmax_len = L;
     }
+    // lengths above the longest query: empty buckets at the end
+    std::fill(B->qstart.begin() + len_max + 1, B->qstart.end(), (uint32_t)pos);
+    std::fill(B->qbbase.begin() + len_max + 1, B->qbbase.end(), bpos);
+    std::fill(B->h_start.p + len_max + 1, B->h_start.p + L1, (uint32_t)pos);
+    std::fill(B->h_bbase.p + len_max + 1, B->h_bbase.p + L1, bpos);
     B->qtotal_bytes = bpos;
     {
         std::vector<uint32_t> cur(B->qstart);
@@ -1076,7 +1088,7 @@ void upload(fpg_batch* B, const uint8_t* qbytes, const uint64_t* qoffsets, uint6
             CK(cudaMemcpyAsync(Q.d_start.p, B->h_start.p, L1 * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
             CK(cudaMemcpyAsync(Q.d_byte_base.p, B->h_bbase.p, L1 * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
         }
-        CK(cudaStreamSynchronize(st));  // caller buffers may be reused once upload returns
+        if (sync) CK(cudaStreamSynchronize(st));  // caller buffers may be reused once upload returns
     });
     if (g_trace) {
         const auto t2 = std::chrono::steady_clock::now();
@@ -1605,7 +1617,7 @@ int fpg_query_batch(fpg_dict* dict, const uint8_t* qbytes, const uint64_t* qoffs
         }
         if (!b) make_batch(dict, &b);
         std::unique_ptr<fpg_batch> own(b);
-        upload(b, qbytes, qoffsets, nq);
+        upload(b, qbytes, qoffsets, nq, false);
         run(b, opt);
         download(b, out);
         std::lock_guard<std::mutex> lk(dict->cache_mu);

@@ -365,20 +365,37 @@ class MatchCSR:
         return len(self.offsets) - 1
 
 
+class _ResultOwner:
+    """Owns a library-allocated fpg_result; frees it when the last numpy view
+    of its arrays goes away (fpg_result_free)."""
+
+    def __init__(self, res: FpgResult):
+        self.res = res
+
+    def __del__(self):
+        try:
+            load_fpg().fpg_result_free(ctypes.byref(self.res))
+        except Exception:  # interpreter shutdown
+            pass
+
+
 def _take_result(res: FpgResult, want_stats: bool):
-    """Copies the library-owned CSR (and stats) into numpy arrays, then frees it."""
+    """Wraps the library-owned CSR (and stats) as numpy arrays without a copy;
+    the result is freed once all of them are released."""
     nq, total = int(res.nq), int(res.total)
+    owner = _ResultOwner(res)
 
-    def take(p, n, dtype):
-        out = np.empty(n, dtype=dtype)
-        if n:
-            ctypes.memmove(out.ctypes.data, ctypes.cast(p, ctypes.c_void_p).value, out.nbytes)
-        return out
+    def view(p, n, ctype, dtype):
+        addr = ctypes.cast(p, ctypes.c_void_p).value
+        if not n or not addr:
+            return np.empty(n, dtype=dtype)
+        buf = (ctype * n).from_address(addr)
+        buf._owner = owner  # keeps the allocation alive as long as the view
+        return np.frombuffer(buf, dtype=dtype)
 
-    offsets = take(res.offsets, nq + 1, np.uint64)
-    ids = take(res.word_ids, total, np.uint32)
-    stats = take(res.stats, nq * 5, np.uint64).reshape(nq, 5) if want_stats else None
-    check(load_fpg().fpg_result_free(ctypes.byref(res)))
+    offsets = view(res.offsets, nq + 1, ctypes.c_uint64, np.uint64)
+    ids = view(res.word_ids, total, ctypes.c_uint32, np.uint32)
+    stats = view(res.stats, nq * 5, ctypes.c_uint64, np.uint64).reshape(nq, 5) if want_stats else None
     return MatchCSR(offsets, ids), stats
 
 
