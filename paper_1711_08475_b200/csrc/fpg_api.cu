@@ -1192,11 +1192,12 @@ void configure_slice(fpg_dict& D, const std::vector<unsigned long long>& hist) {
         if (hist[c] && D.params.slot[c] < 0) others.push_back(c);
     std::stable_sort(others.begin(), others.end(), [&](int a, int b) { return hist[a] > hist[b]; });
     auto snap = [](size_t v) { return v == 0 ? 0 : v <= 8 ? 8 : v <= 12 ? 12 : 16; };
-    // W = 32 keeps two slabs per lane (NPT <= 40) with at most 8 sig' fields.
-    // No sig' when it cannot pay (measured): <= 4 other
+    // W = 32 takes at most 12 sig' fields: NPT = 44 leaves one slab per lane,
+    // yet every W = 32 cell of configs 3 and 5 ran 4-10% faster than with 8
+    // (fewer candidates).  No sig' when it cannot pay (measured): <= 4 other
     // symbols, or a 64-bit count fingerprint (16 four-bit fields already
     // leave few candidates).
-    int S = snap(std::min<size_t>(others.size(), D.scheme.width == 32 ? 8 : 16));
+    int S = snap(std::min<size_t>(others.size(), D.scheme.width == 32 ? 12 : 16));
     if (others.size() <= 4 || (D.scheme.width == 64 && D.scheme.variant == FPG_COUNT)) S = 0;
     if (const char* sb = std::getenv("FPG_SIGP_BITS")) S = snap((size_t)std::max(0, std::atoi(sb)));
     std::memset(D.params.sigbit, -1, sizeof(D.params.sigbit));
