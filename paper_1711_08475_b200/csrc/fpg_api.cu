@@ -517,6 +517,22 @@ fpg_dict::~fpg_dict() {
 
 namespace {
 
+// Host-side assembly of large results in parallel: [0, n) cut into one range
+// per thread (at least `grain` items each, up to the host's cores).  The
+// threads also take the first-touch page faults of freshly allocated output.
+template <class F>
+void parallel_ranges(uint64_t n, uint64_t grain, F&& f) {
+    static const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const uint64_t t = std::max<uint64_t>(1, std::min<uint64_t>(hw, n / std::max<uint64_t>(grain, 1)));
+    if (t == 1) {
+        f(uint64_t(0), n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (uint64_t i = 0; i < t; ++i) th.emplace_back([&, i] { f(n * i / t, n * (i + 1) / t); });
+    for (auto& x : th) x.join();
+}
+
 template <class F>
 void for_each_shard(size_t n, F&& f) {
     if (n == 1) {
@@ -1125,20 +1141,28 @@ void download(fpg_batch* B, fpg_result* out) {
     if (B->sb.size() == 1) {
         ShardBatch& S = *B->sb[0];
         std::memcpy(out->offsets, S.h_offsets.p, sizeof(uint64_t) * (nq + 1));
-        if (total) std::memcpy(out->word_ids, S.h_ids.p, sizeof(uint32_t) * total);
+        parallel_ranges(total, 1u << 20, [&](uint64_t lo, uint64_t hi) {
+            if (hi > lo) std::memcpy(out->word_ids + lo, S.h_ids.p + lo, sizeof(uint32_t) * (hi - lo));
+        });
     } else {
         // Shards own ascending contiguous id ranges: concatenating each query's
         // shard rows in shard order yields ascending ids (oracle order).
         uint64_t pos = 0;
         for (uint64_t q = 0; q < nq; ++q) {
             out->offsets[q] = pos;
-            for (auto& s : B->sb) {
-                const uint64_t a = s->h_offsets.p[q], b = s->h_offsets.p[q + 1];
-                if (b > a) std::memcpy(out->word_ids + pos, s->h_ids.p + a, sizeof(uint32_t) * (b - a));
-                pos += b - a;
-            }
+            for (auto& s : B->sb) pos += s->h_offsets.p[q + 1] - s->h_offsets.p[q];
         }
         out->offsets[nq] = pos;
+        parallel_ranges(nq, 1u << 14, [&](uint64_t qlo, uint64_t qhi) {
+            for (uint64_t q = qlo; q < qhi; ++q) {
+                uint64_t at = out->offsets[q];
+                for (auto& s : B->sb) {
+                    const uint64_t a = s->h_offsets.p[q], b = s->h_offsets.p[q + 1];
+                    if (b > a) std::memcpy(out->word_ids + at, s->h_ids.p + a, sizeof(uint32_t) * (b - a));
+                    at += b - a;
+                }
+            }
+        });
     }
     if (stats) {
         out->stats = static_cast<uint64_t*>(std::malloc(FPG_NSTATS * sizeof(uint64_t) * std::max<uint64_t>(nq, 1)));
@@ -1159,18 +1183,20 @@ void download(fpg_batch* B, fpg_result* out) {
                 comp_of[lq] = c;
             }
         const size_t G = B->sb.size();
-        for (uint64_t q = 0; q < nq; ++q) {
-            uint64_t surv = 0;
-            for (size_t g = 0; g < G; ++g) surv += B->sb[g]->h_qsurv.p[q];
-            const uint64_t comp = comp_of[B->qlen[q]];
-            uint64_t* st = out->stats + FPG_NSTATS * q;
-            const uint64_t verified = o.use_filter ? surv : comp;
-            st[FPG_STAT_COMPARED] = N;
-            st[FPG_STAT_REJECTED_BY_LENGTH] = N - comp;
-            st[FPG_STAT_REJECTED_BY_FINGERPRINT] = comp - verified;
-            st[FPG_STAT_VERIFIED] = verified;
-            st[FPG_STAT_MATCHES] = out->offsets[q + 1] - out->offsets[q];
-        }
+        parallel_ranges(nq, 1u << 16, [&](uint64_t qlo, uint64_t qhi) {
+            for (uint64_t q = qlo; q < qhi; ++q) {
+                uint64_t surv = 0;
+                for (size_t g = 0; g < G; ++g) surv += B->sb[g]->h_qsurv.p[q];
+                const uint64_t comp = comp_of[B->qlen[q]];
+                uint64_t* st = out->stats + FPG_NSTATS * q;
+                const uint64_t verified = o.use_filter ? surv : comp;
+                st[FPG_STAT_COMPARED] = N;
+                st[FPG_STAT_REJECTED_BY_LENGTH] = N - comp;
+                st[FPG_STAT_REJECTED_BY_FINGERPRINT] = comp - verified;
+                st[FPG_STAT_VERIFIED] = verified;
+                st[FPG_STAT_MATCHES] = out->offsets[q + 1] - out->offsets[q];
+            }
+        });
     }
     if (g_trace) {
         const auto t2 = std::chrono::steady_clock::now();
