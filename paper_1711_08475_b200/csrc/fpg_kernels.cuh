@@ -3,15 +3,18 @@
 //   K0 k_hist256    byte histogram (sig' ranking, letter selection)
 //   K1 k_build      one thread per string: fingerprint (reference build(),
 //                   fingerprint.hpp:216-284, generalised to W bits), sig'
-//                   code, weight, and the bytes copied into the length-bucketed
-//                   16-byte-stride layout.  k_weight_keys / k_lengths feed the
-//                   (length, weight) sort of the dictionary.
-//   K1b k_planes    bit-sliced planes per 32-word slab (fpg_slice.cuh)
+//                   code, group weights, and the bytes copied into the
+//                   length-bucketed 16-byte-stride layout.  k_weight_keys /
+//                   k_lengths feed the (length, group weights) sort of the
+//                   dictionary.
+//   K1b k_planes    bit-sliced planes and group-weight box per 32-word slab
+//                   (fpg_slice.cuh)
 //   K2 k_slice      the bit-sliced filter + k <= 1 verifier (fpg_slice.cuh);
 //      k_scan       the generic per-pair XOR + POPC filter (fpg_scan.cuh):
 //                   fields wider than 4 bits, k >= 2 (banded verifier)
 //   K4 k_seg_scatter / k_seg_sort   CSR: keys scattered into per-query
-//                   segments, segments of <= 32 warp-sorted (larger ones: CUB
+//                   segments (sorted word positions mapped to input-order
+//                   ids), segments of <= 32 warp-sorted (larger ones: CUB
 //                   segmented sort, launched by the host)
 #pragma once
 

@@ -1,8 +1,8 @@
 // fpg_slice.cuh -- K2 as a bit-sliced scan (sm_100a): no POPC on the pair path.
 //
-// Layout.  The words of one dictionary length bucket, sorted by fingerprint
-// weight (input order within a weight), are cut into slabs of 32 consecutive
-// words.  A slab is stored as NPT 32-bit planes:
+// Layout.  The words of one dictionary length bucket, sorted by their four
+// group weights (input order within equal keys), are cut into slabs of 32
+// consecutive words.  A slab is stored as NPT 32-bit planes:
 // plane b holds bit b of the 32 words' comparison codes (K1b k_planes).
 // Planes 0..NP-1 are the scheme fingerprint bits in the reference layout
 // (fingerprint.hpp:48-56, :138-147: NF fields of FW bits above EXTRA one-bit
@@ -18,12 +18,21 @@
 //   x_b   = plane_b XOR query_bit_b         one IMAD: plane * s + m with
 //                                           (s, m) = (1, 0) or (-1, ~0), FMA pipe
 //   x_f   = OR of the field's x_b           (LOP3, fields wider than 1 bit)
-//   c2 |= c1 & x_f; c1 |= c0 & x_f; c0 |= x_f   three LOP3: saturating
-//                                           counters, c_i = "F >= i+1" per word
-// so bit w of c2 (c0 for k = 0) says word w is rejected.  Per 32 pairs that
-// is 3 ALU ops per 1-bit field (4 per wider field) and one IMAD per plane:
-// 1.0-1.5 ALU ops per comparison for a 16-bit fingerprint, against the POPC
-// pipe's 16/clk/SM bound of a per-pair XOR + POPC.
+//   carry-save counter F = o + 2 t + 4 [f], fields entering four at a time:
+//     o1 = o ^ x1 ^ x2, k1 = maj(o, x1, x2); o = o1 ^ x3 ^ x4,
+//     k2 = maj(o1, x3, x4); f |= maj(t, k1, k2); t ^= k1 ^ k2   (7 LOP3)
+// so bit w of f | (t & o) (k = 1: F >= 3; f | t | o for k = 0) says word w
+// is rejected.  Per 32 pairs that is 7/4 ALU ops per 1-bit field plus the
+// field ORs, and one IMAD per plane: about 1.6 ALU ops per comparison for
+// count-16 with 16 sig' fields, against the POPC pipe's 16/clk/SM bound of a
+// per-pair XOR + POPC.
+//
+// Scheduling.  A tile is (<= 128 queries) x (<= 32 slab groups of SL rows of
+// 32 slabs) of one word length.  The CTA writes the tile's query masks to
+// shared memory once; its warps then claim slab groups from a shared counter
+// (warp w's first group prefetched during the setup), load the group's planes
+// into registers, build the group's query list through the weight window and
+// scan it two queries per step.
 //
 // Weight window.  sum_g |gw_g(q) - gw_g(x)| <= F_D over 4 field groups
 // (fp_gweight), so a warp skips the queries whose group weights are more than
@@ -43,8 +52,8 @@
 // Candidates (rare) go to a lane-private queue in shared memory as
 // (query, slab, 32-bit word mask) and are byte-verified at k <= 1
 // (edit_distance.hpp:18-64) in warp-wide batches; matches leave as
-// (query id << 32 | word id) keys through per-warp output chunks (OutChunk)
-// for K4.
+// (query id << 32 | sorted word position) keys through per-warp output
+// chunks (OutChunk) for K4, which maps positions to input-order ids.
 #pragma once
 
 #include <cstdint>
