@@ -403,9 +403,12 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 if (i < NF) {
                     const int b0 = EXTRA + FW * i;
                     uint32_t x = qxor(pl[r][b0], FPG_QS(h, b0), FPG_QM(h, b0));
-                    if constexpr (FW == 2) {
-                        // x | (p ^ m) is one LOP3: the second plane needs no IMAD
-                        x |= pl[r][b0 + 1] ^ FPG_QM(h, b0 + 1);
+                    if constexpr (FW % 2 == 0) {
+                        // even widths: the last plane joins the OR as x | (p ^ m),
+                        // one LOP3 either way, so its query XOR needs no IMAD
+#pragma unroll
+                        for (int u = 1; u + 1 < FW; ++u) x |= qxor(pl[r][b0 + u], FPG_QS(h, b0 + u), FPG_QM(h, b0 + u));
+                        x |= pl[r][b0 + FW - 1] ^ FPG_QM(h, b0 + FW - 1);
                     } else {
 #pragma unroll
                         for (int u = 1; u < FW; ++u) x |= qxor(pl[r][b0 + u], FPG_QS(h, b0 + u), FPG_QM(h, b0 + u));
