@@ -47,9 +47,10 @@ ALU_PER_CLK_PER_SM = 64   # LOP3 issue: 16 lanes/clk/SMSP (B300_MICROARCH.md "Pi
 def ops_per_comparison(scheme, sig_fields: int) -> float:
     """LOP3 per comparison of the bit-sliced test (fpg_slice.cuh): per 32-word
     slab, the ORs folding a multi-bit field's planes (1 for 2-3 bits, 2 for 4
-    bits), then the carry-save counter: 7 per four field bits, 4 per
-    remaining pair or single, counted separately over the scheme fields and
-    the sig' fields (one-bit), plus 1 for the reject mask."""
+    bits), then the carry-save counter: 6 per four field bits plus one
+    fours-carry OR per two such quads, 4 per remaining pair or single, counted
+    separately over the scheme fields and the sig' fields (one-bit), plus 1
+    for the reject mask."""
     v, w = scheme.variant().name, scheme.width()
     if v == "Count":
         fw, extra = scheme.bits_per_count(), 0
@@ -60,8 +61,9 @@ def ops_per_comparison(scheme, sig_fields: int) -> float:
         fw, extra = 1, 0
     nf = (w - extra) // fw
 
-    def csa(n: int) -> int:
-        return 7 * (n // 4) + 4 * ((n % 4 + 1) // 2)
+    def csa(n: int) -> int:  # 6 per quad + one carry OR per two quads, 4 per pair / single
+        q4 = n // 4
+        return 6 * q4 + (q4 + 1) // 2 + 4 * ((n % 4 + 1) // 2)
 
     ors = nf * (0 if fw == 1 else 1 if fw <= 3 else 2)
     return (ors + csa(nf + extra) + csa(sig_fields) + 1) / 32.0

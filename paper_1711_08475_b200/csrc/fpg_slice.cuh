@@ -418,13 +418,19 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 const int b = i < NF + EXTRA ? i - NF : NP + (i - NF - EXTRA);
                 return qxor(pl[r][b], FPG_QS(h, b), FPG_QM(h, b));
             };
-            auto add4 = [&](int h, int r, uint32_t x1, uint32_t x2, uint32_t x3, uint32_t x4) {
+            // mode 0: f |= m; 1: m is held back (pm); 2: f |= pm | m (one LOP3
+            // for two quads' fours carries)
+            uint32_t pm[NQ][SLX];
+            auto add4 = [&](int h, int r, uint32_t x1, uint32_t x2, uint32_t x3, uint32_t x4, int mode) {
                 const uint32_t o = co[h][r];
                 const uint32_t o1 = o ^ x1 ^ x2, k1 = maj3(o, x1, x2);
                 const uint32_t k2 = maj3(o1, x3, x4);
                 co[h][r] = o1 ^ x3 ^ x4;
                 const uint32_t t = ct[h][r];
-                cf[h][r] |= maj3(t, k1, k2);
+                const uint32_t m = maj3(t, k1, k2);
+                if (mode == 1) pm[h][r] = m;
+                else if (mode == 2) cf[h][r] |= pm[h][r] | m;
+                else cf[h][r] |= m;
                 ct[h][r] = t ^ k1 ^ k2;
             };
             auto add2 = [&](int h, int r, uint32_t x1, uint32_t x2) {
@@ -438,12 +444,15 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 constexpr int I0 = decltype(i0c)::value, I1 = decltype(i1c)::value;
                 constexpr int N4 = (I1 - I0) / 4 * 4;
 #pragma unroll
-                for (int i = I0; i < I0 + N4; i += 4)
+                for (int i = I0; i < I0 + N4; i += 4) {
+                    const int q = (i - I0) / 4;  // quad index: pairs of quads share the carry OR
+                    const int mode = (q & 1) ? 2 : (q + 1 < N4 / 4 ? 1 : 0);
 #pragma unroll
                     for (int h = 0; h < NQ; ++h)
 #pragma unroll
                         for (int r = 0; r < SLX; ++r)
-                            add4(h, r, fbit(h, r, i), fbit(h, r, i + 1), fbit(h, r, i + 2), fbit(h, r, i + 3));
+                            add4(h, r, fbit(h, r, i), fbit(h, r, i + 1), fbit(h, r, i + 2), fbit(h, r, i + 3), mode);
+                }
 #pragma unroll
                 for (int i = I0 + N4; i < I1; i += 2)
 #pragma unroll
