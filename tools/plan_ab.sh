@@ -1,3 +1,4 @@
+# A/B of the K2 tile shape for small batches on config 2: PLANS="gpw,q ..." (FPG_TILE_GPW / FPG_TILE_Q).
 mkdir -p gpurun_out/ab
 timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/ab/pt.log 2>&1; echo pytest_rc=$?; tail -1 gpurun_out/ab/pt.log
 for v in ${PLANS:-2,32 4,16 4,32 1,64}; do set -- ${v/,/ }
