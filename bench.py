@@ -2,26 +2,39 @@
 """Benchmark of the k=1 fingerprint-filtered query x dictionary scan.
 
 Metric (BASELINE.json:2): logical query x word comparisons per second,
-Q * N per batch (the reference's pair denominator, bench.hpp:157-161),
-whole job over all GPUs.  Default workload = config 2 (BASELINE.json:8,
-configs[1]): 1e6 uniform a-z words, L~U[4,20], 10,000 queries, count-16
-fingerprints (b=2, 8 common letters), Levenshtein, k=1, length prefilter on,
-per-query QueryStats on.  One step = one batch through the scan.
+Q * N per batch (the reference's pair denominator, bench.hpp:157-161), whole
+job over all GPUs.  Default workload = config 5 (BASELINE.json:11, the
+configuration the metric is quoted on "at 1/2/4/8 B200"): 64,000,000 uniform
+a-z words, L~U[4,16], one batch of 1,000,000 queries (50% one edit, 50%
+random), cell 0 = occurrence-16 fingerprints, Hamming, k = 1, per-query
+QueryStats on (run_pass collects them, bench.hpp:80-90).  One step = one
+batch through the scan.  Letters are selected over the whole 64M-word
+dictionary and query sources are drawn from all of it.
 
-Multi-GPU (torchrun, one process per GPU): weak scaling.  Rank r owns
-dictionary shard r = words [r*N, (r+1)*N) of config 2's seeded stream (shard
-0 IS config 2's dictionary); every rank scans the same 10,000 queries;
-word ids are rebased by r*N; results land in each rank's host memory.
-No data-path collective.  Times are CUDA-event device times, max over ranks.
+Scaling is STRONG for config 5 (BASELINE: one 64M-word dictionary "sharded
+evenly across 8xB200"): with N GPUs each owns 64M/N words (contiguous
+input-order id ranges) and scans the same 1M queries.  Other configs run
+weak scaling (each GPU holds a copy-sized shard of the config's stream).
 
-  value  device-resident: inputs already in HBM (fpg_batch_run only)
-  e2e    through the public C ABI call fpg_query_batch with pinned host
-         buffers: H2D of the queries, scan, D2H of the CSR + stats
+  --gpus N without torchrun: ONE process drives N GPUs (devices 0..N-1)
+      through GpuFingerprintedDictionary(devices=...); libfpg.so gathers the
+      shard rows on the host inside the e2e call.  Fails loudly if fewer
+      than N devices exist (FPG_BENCH_DEVICES="0,0" overrides, for tests).
+  torchrun --nproc-per-node N ... --gpus N: one process per GPU (asserted
+      WORLD_SIZE == N); rank r owns shard r; the e2e step gathers the ranks'
+      device-resident CSRs to rank 0 over NCCL and merges them there on the
+      GPU (sharding.query_batch_distributed).
+
+  value  device-resident: inputs already in HBM, CUDA-event time of
+         fpg_batch_run (K1 on the queries, K2, K4), max over shards / ranks
+  e2e    through the public API with pinned host buffers: H2D of the
+         queries, scan, gather + merge of the shards, D2H of the CSR (+
+         QueryStats on one process), wall time, max over ranks
 
 --impl reference runs the reference's own CPU implementation
 (oracle/_ref/libfpref.so: /root/reference headers, FingerprintedDictionary::
 query_into) on all host threads over a bounded query sample of the same
-workload, on rank 0 only.
+workload, on rank 0 only; libfpg.so is never loaded in that process.
 """
 from __future__ import annotations
 
@@ -40,8 +53,19 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+METRIC = "k=1 query x word comparisons/s (logical Q*N)"
 POPC_PER_CLK_PER_SM = 16  # measured: tools/microbench/intpipe.cu (profiles/r01_phase0.txt)
-ALU_PER_CLK_PER_SM = 64   # LOP3 issue: 16 lanes/clk/SMSP (B300_MICROARCH.md "Pipe rates")
+L2_NOTE = "flushed between timed steps (256 MB write > 126 MB L2)"
+
+
+def alu_peak():
+    """(LOP3 thread-ops per clk per SM, basis) from the committed B200
+    microbenchmark (tools/microbench/alupipe.cu -> profiles/alu_peak.json)."""
+    try:
+        rec = json.loads((ROOT / "profiles" / "alu_peak.json").read_text())
+        return float(rec["lop3_per_clk_per_sm"]), rec["basis"]
+    except (OSError, ValueError, KeyError):
+        return 64.0, "unmeasured: 16 lanes/clk/SMSP (B300_MICROARCH.md pipe rates)"
 
 
 def ops_per_comparison(scheme, sig_fields: int) -> float:
@@ -83,14 +107,15 @@ def profiled_traffic(workload: str, cell: str):
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--cell", type=int, default=0, help="index into corpus.CELLS[config]")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg (profiling runs)")
     return ap.parse_args()
 
 
@@ -152,18 +177,46 @@ def dist_env():
     return world, rank, local
 
 
-def workload(cfg: int, cell: int, rank: int, world: int):
-    from paper_1711_08475_b200.corpus import CELLS, CONFIGS, generate_dictionary, generate_queries, make_scheme
+class Workload:
+    """The config's whole dictionary and query batch (seeded generators), the
+    scheme with letters chosen over the whole dictionary, and the shard this
+    process owns."""
 
-    c = CONFIGS[cfg]
-    n = c.n_words // world if cfg == 5 else c.n_words  # cfg5: strong (the 64M dict split); else weak
-    first = rank * n
-    base_blob, base_offs = generate_dictionary(cfg, n=n if cfg != 5 else min(n, 8_000_000), first=0)
-    blob, offs = (base_blob, base_offs) if first == 0 and cfg != 5 else generate_dictionary(cfg, n=n, first=first)
-    qblob, qoffs = generate_queries(cfg, base_blob, base_offs, nq=c.n_queries)
-    variant, width, b, p, metric = CELLS[cfg][cell]
-    scheme = make_scheme(base_blob, variant, width, b, p)  # letters from the base (config) dictionary
-    return c, blob, offs, qblob, qoffs, scheme, metric, first, n
+    def __init__(self, cfg: int, cell: int, parts: int = 1, part: int = 0):
+        from paper_1711_08475_b200.corpus import CELLS, CONFIGS, generate_dictionary, generate_queries, make_scheme
+        from paper_1711_08475_b200.sharding import shard_bounds, shard_of
+
+        self.cfg, self.cell, self.c = cfg, cell, CONFIGS[cfg]
+        self.strong = cfg == 5  # config 5: one dictionary split over the GPUs
+        n_all = self.c.n_words if self.strong else self.c.n_words * parts
+        t0 = time.perf_counter()
+        self.blob, self.offs = generate_dictionary(cfg, n=n_all)
+        self.qblob, self.qoffs = generate_queries(cfg, self.blob, self.offs, nq=self.c.n_queries)
+        variant, width, b, p, self.metric = CELLS[cfg][cell]
+        self.scheme = make_scheme(self.blob, variant, width, b, p)  # letters over the WHOLE dictionary
+        self.setup_s = time.perf_counter() - t0
+        self.n_all = n_all
+        self.lo, self.hi = shard_bounds(n_all, parts, part)
+        self.sblob, self.soffs = shard_of(self.blob, self.offs, self.lo, self.hi) if parts > 1 else (self.blob, self.offs)
+        self.nq = len(self.qoffs) - 1
+        self.mean_len = float(self.offs[-1]) / max(n_all, 1)
+        self.qmean_len = float(self.qoffs[-1]) / max(self.nq, 1)
+
+    def cell_name(self) -> str:
+        from paper_1711_08475_b200.corpus import CELLS
+
+        v, w, b, p, m = CELLS[self.cfg][self.cell]
+        extra = f" b={b}" if v.name == "Count" else (f" p={p}" if v.name == "Position" else "")
+        return f"{v.name}-{w}{extra} {m.name} k=1"
+
+    def config(self, n_gpus: int) -> dict:
+        """The `config` object of both arms' JSON lines (identical keys)."""
+        return {"workload": f"config{self.cfg}", "cell": self.cell_name(), "n_words": self.n_all,
+                "n_queries": self.nq, "mean_word_len": round(self.mean_len, 3),
+                "mean_query_len": round(self.qmean_len, 3), "k": 1, "length_prefilter": True,
+                "query_stats": True, "letters": self.scheme.letters().symbols().decode("latin-1"),
+                "l2": L2_NOTE, "parallelism": f"dict-shard x{n_gpus}",
+                "scaling_mode": "strong" if self.strong else "weak"}
 
 
 _PINNED = []  # owners of pinned host storage
@@ -202,209 +255,296 @@ def reduce_sum(x: float, world: int) -> float:
     return float(t.item())
 
 
-def cpu_reference_rate(blob, offs, qblob, qoffs, scheme, metric, budget_s: float, threads: int):
-    """Reference CPU scan (oracle/_ref, else the C restatement) on a bounded
-    query sample; returns (pairs/s, kind, sample description, threads)."""
+def cpu_reference_rate(w: Workload, budget_s: float, threads: int):
+    """Reference CPU scan (oracle/_ref, else the C restatement) of the whole
+    dictionary on a bounded, evenly spaced query sample; returns (pairs/s,
+    kind, sample description).  Letters and scheme are the GPU arm's."""
     from oracle.oracle import Oracle, Reference, oscheme
     from paper_1711_08475_b200.corpus import subsample
 
-    n = len(offs) - 1
-    nq = len(qoffs) - 1
+    blob, offs, qblob, qoffs, scheme, metric = w.blob, w.offs, w.qblob, w.qoffs, w.scheme, w.metric
+    n, nq = len(offs) - 1, len(qoffs) - 1
     if Reference.available():
         ref = Reference()
+        t0 = time.perf_counter()
         d = ref.dictionary(blob, offs, int(scheme.variant()), scheme.letters().symbols(),
                            scheme.bits_per_count() or 2, scheme.bits_per_position() or 3)
+        build_s = time.perf_counter() - t0
         kind = "reference"
         run = lambda qb, qo: d.query_batch(qb, qo, int(metric), 1, True, True, threads)  # noqa: E731
     else:
         orc = Oracle()
         osch = oscheme(int(scheme.variant()), scheme.letters().symbols(), scheme.width(),
                        scheme.bits_per_count() or 2, scheme.bits_per_position() or 3)
-        kind = "port"
+        kind, build_s = "port", 0.0
         run = lambda qb, qo: orc.query_batch(blob, offs, qb, qo, osch, int(metric), 1, True, True, threads)  # noqa: E731
-    # calibrate on a small sample, then size the timed sample to the budget
-    step = max(1, nq // (4 * threads))
-    qb, qo, idx = subsample(qblob, qoffs, step)
-    t0 = time.perf_counter()
-    run(qb, qo)
-    dt = time.perf_counter() - t0
-    per_query = dt / max(len(idx), 1)
-    want = int(min(nq, max(threads, budget_s / max(per_query, 1e-9))))
-    step = max(1, nq // want)
-    qb, qo, idx = subsample(qblob, qoffs, step)
-    t0 = time.perf_counter()
-    run(qb, qo)
-    dt = time.perf_counter() - t0
-    pairs = len(idx) * n
-    sample = f"every {step}th query ({len(idx)} of {nq}) x all {n} words, one pass, {dt:.1f} s"
-    return pairs / dt, kind, sample, dt
+
+    def rate(budget):
+        # calibrate on a small sample, then size the timed sample to the budget
+        step = max(1, nq // (2 * threads))
+        qb, qo, idx = subsample(qblob, qoffs, step)
+        t0 = time.perf_counter()
+        run(qb, qo)
+        per_query = (time.perf_counter() - t0) / max(len(idx), 1)
+        want = int(min(nq, max(threads, budget / max(per_query, 1e-9))))
+        step = max(1, nq // want)
+        qb, qo, idx = subsample(qblob, qoffs, step)
+        t0 = time.perf_counter()
+        run(qb, qo)
+        dt = time.perf_counter() - t0
+        sample = (f"every {step}th query ({len(idx)} of {nq}) x all {n} words, one pass, {dt:.1f} s "
+                  f"(reference dictionary construction {build_s:.1f} s, untimed)")
+        return len(idx) * n / dt, sample
+
+    return rate, kind
+
+
+def reference_arm(args) -> None:
+    """The reference's CPU scan on all host threads, rank 0 only."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_1711_08475_b200 import _lib
+
+    w = Workload(args.config, args.cell)
+    threads = _lib.host_threads()
+    rate, kind = cpu_reference_rate(w, 0, threads)
+    rates, sample = [], ""
+    per_step = max(2.0, 60.0 / max(args.steps, 1))
+    for i in range(args.warmup + args.steps):
+        r, sample = rate(per_step if i >= args.warmup else 1.0)
+        if i >= args.warmup:
+            rates.append(r)
+    assert _lib._fpg is None, "the reference arm must not load libfpg.so"
+    value = statistics.mean(rates)
+    line = {"metric": METRIC, "value": value, "unit": "comparisons/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * w.nq * w.n_all / value,  # one full batch at the sampled rate
+            "higher_is_better": True, "scaling": "strong" if w.strong else "weak", "vs_baseline": None,
+            "dtype": "u8", "data": f"synthetic (seeded generator, config {args.config}; see corpus.py)",
+            "config": w.config(args.gpus),
+            "cpu_baseline": {"value": value, "unit": "comparisons/s", "cores": threads, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "comparisons/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "libfpg_loaded": False}
+    print(json.dumps(line), flush=True)
+
+
+def bench_devices(n: int) -> tuple[int, ...]:
+    """Devices of the one-process N-GPU run: FPG_BENCH_DEVICES ("0,0") or
+    0..n-1; fails loudly when fewer than n GPUs are present."""
+    import torch
+
+    env = os.environ.get("FPG_BENCH_DEVICES")
+    if env:
+        devs = tuple(int(x) for x in env.split(","))
+        if len(devs) != n:
+            raise SystemExit(f"FPG_BENCH_DEVICES lists {len(devs)} devices, --gpus is {n}")
+        return devs
+    have = torch.cuda.device_count()
+    if have < n:
+        raise SystemExit(f"bench.py --gpus {n}: only {have} CUDA device(s) visible "
+                         "(set FPG_BENCH_DEVICES to place several shards on one device)")
+    return tuple(range(n))
 
 
 def main():
     args = parse()
-    world, rank, local = dist_env()
-    from paper_1711_08475_b200._lib import host_threads
-
     if args.impl == "reference":
-        if rank != 0:
-            return
-        c, blob, offs, qblob, qoffs, scheme, metric, first, n = workload(args.config, args.cell, 0, 1)
-        threads = host_threads()
-        rates = []
-        sample = kind = ""
-        for i in range(args.warmup + args.steps):
-            budget = max(2.0, 60.0 / (args.warmup + args.steps)) if i >= args.warmup else 1.0
-            r, kind, sample, _ = cpu_reference_rate(blob, offs, qblob, qoffs, scheme, metric, budget, threads)
-            if i >= args.warmup:
-                rates.append(r)
-        value = statistics.mean(rates)
-        line = {"metric": "k=1 query x word comparisons/s (logical Q*N)", "value": value, "unit": "comparisons/s",
-                "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": 1e3 * c.n_queries * n / value,  # one full batch at the sampled rate "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "u8", "data": "synthetic (seeded generator, config %d)" % args.config,
-                "config": {"workload": f"config{args.config}", "cell": _cell_name(args.config, args.cell),
-                           "n_words": n, "n_queries": c.n_queries},
-                "cpu_baseline": {"value": value, "unit": "comparisons/s", "cores": threads, "kind": kind,
-                                 "sample": sample},
-                "e2e": {"value": value, "unit": "comparisons/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
+        reference_arm(args)
         return
-
+    world, rank, local = dist_env()
     import torch
 
     if world > 1:
         import torch.distributed as dist
 
+        if world != args.gpus:
+            raise SystemExit(f"torchrun WORLD_SIZE={world} but --gpus {args.gpus}")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = local if world > 1 else 0
+        devices = (local,)
+    else:
+        devices = bench_devices(args.gpus)
+    n_gpus = args.gpus
 
     from paper_1711_08475_b200 import GpuFingerprintedDictionary, QueryOptions
+    from paper_1711_08475_b200._lib import host_threads
 
-    c, blob, offs, qblob, qoffs, scheme, metric, first, n = workload(args.config, args.cell, rank, world)
-    nq = len(qoffs) - 1
-    opt = QueryOptions(metric, 1, True, True)
-    d = GpuFingerprintedDictionary((blob, offs), scheme, devices=(dev,), id_base=first, keep_words=False)
+    w = Workload(args.config, args.cell, parts=world, part=rank)
+    opt = QueryOptions(w.metric, 1, True, True)
+    dev0 = devices[0]
+    torch.cuda.set_device(dev0)
+    d = GpuFingerprintedDictionary((w.sblob, w.soffs), w.scheme, devices=devices, id_base=w.lo, keep_words=False)
     build_s = d.build_seconds()
+    nsh = len(devices)
     batch = d.batch()
-    batch.upload(qblob, qoffs)
+    batch.upload(w.qblob, w.qoffs)
     flush = None
     if not args.no_flush:
-        flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
+        flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev0}")
 
     def barrier():
-        torch.cuda.synchronize(dev)
+        for dv in set(devices):
+            torch.cuda.synchronize(dv)
         if world > 1:
             torch.distributed.barrier()
 
     for _ in range(args.warmup):
         batch.run(opt, want_stats=True)
-    clocks = Clocks(dev)
+    clocks = Clocks(dev0)
     clocks.start()
-    run_ms, filt_ms, launches, executed, survivors, candidates, scanned = [], [], 0, 0, 0, 0, 0
+    step_ms, shard_ms, filt_ms, launches = [], [], [], 0
     barrier()
     clocks.open()
     for _ in range(args.steps):
         if flush is not None:
             flush.zero_()  # L2 flush (256 MB > 126 MB L2), outside the event-timed run
-            torch.cuda.synchronize(dev)
+            torch.cuda.synchronize(dev0)
         batch.run(opt, want_stats=True)
-        t = batch.timing()
-        run_ms.append(t["run_ms"])
-        filt_ms.append(t["filter_ms"])
-        launches += t["launches"]
-        executed, survivors, candidates = t["executed_pairs"], t["survivors"], t["candidates"]
-        scanned = t["scanned_pairs"]
+        ts = [batch.timing(s) for s in range(nsh)]
+        step_ms.append(max(t["run_ms"] for t in ts))  # shards run concurrently: the slowest one
+        shard_ms.append([t["run_ms"] for t in ts])
+        filt_ms.append([t["filter_ms"] for t in ts])
+        launches += sum(t["launches"] for t in ts)
     barrier()
     clocks.close()
     clk = clocks.stop()
+    t_last = [batch.timing(s) for s in range(nsh)]
     csr, st = batch.download()
-    total_ms = reduce_max(sum(run_ms), world)
+    total_ms = reduce_max(sum(step_ms), world)
     ms_per_step = total_ms / args.steps
-    logical_pairs_all = reduce_sum(float(nq) * n, world)  # Q x N over all shards
+    logical_pairs_all = float(w.nq) * w.n_all  # Q x N of the whole (sharded or replicated) job
     value = logical_pairs_all * args.steps / (total_ms / 1e3)
 
-    # e2e: public C ABI call with pinned host buffers (H2D + scan + D2H inside)
-    qb_p, qo_p = pinned_copy(qblob), pinned_copy(qoffs)
-    for _ in range(max(1, args.warmup)):
-        d.query_batch((qb_p, qo_p), opt, per_query_stats=True)
-    barrier()
-    e2e_s, e2e_csr = 0.0, None
-    for _ in range(args.steps):
-        if flush is not None:
-            flush.zero_()
-            torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()  # the call is blocking: H2D, scan, D2H, CSR assembly
-        e2e_csr, _ = d.query_batch((qb_p, qo_p), opt, per_query_stats=True)
-        e2e_s += time.perf_counter() - t0
-    barrier()
-    e2e_s = reduce_max(e2e_s, world)
-    e2e_value = logical_pairs_all * args.steps / e2e_s
+    # e2e through the public API with pinned host buffers
+    qb_p, qo_p = pinned_copy(w.qblob), pinned_copy(w.qoffs)
+    e2e = None
+    if not args.no_e2e:
+        gather = []
+        if world == 1:
+            def e2e_step():
+                batch.upload(qb_p, qo_p)  # H2D
+                batch.run(opt, want_stats=True)
+                out = batch.download()  # D2H + host gather of the shard rows + QueryStats
+                gather.append(batch.host_ms()["assemble_ms"])
+                return out[0]
+        else:
+            cap = int(csr.offsets[-1]) if csr.offsets is not None else 0
+            h_out = (torch.empty(w.nq + 1, dtype=torch.int64, pin_memory=True),
+                     torch.empty(max(int(reduce_sum(cap, world)) * 2, 1), dtype=torch.int32, pin_memory=True))
 
-    assert np.array_equal(e2e_csr.word_ids, csr.word_ids), "e2e and staged results differ"
-    h2d = int(qblob.nbytes + qoffs.nbytes)
-    d2h = int(8 * (nq + 1) + 4 * int(csr.offsets[-1]) + 4 * nq)
+            def e2e_step():
+                batch.upload(qb_p, qo_p)  # H2D
+                batch.run(opt, want_stats=True)
+                t1 = time.perf_counter()
+                out = _gather_merge(batch, h_out)  # NCCL gather, device merge, D2H on rank 0
+                gather.append((time.perf_counter() - t1) * 1e3)
+                return out
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        barrier()
+        e2e_s, last = 0.0, None
+        for _ in range(args.steps):
+            if flush is not None:
+                flush.zero_()
+                torch.cuda.synchronize(dev0)
+            if world > 1:
+                torch.distributed.barrier()
+            t0 = time.perf_counter()
+            last = e2e_step()
+            e2e_s += time.perf_counter() - t0
+        barrier()
+        e2e_s = reduce_max(e2e_s, world)
+        if rank == 0 and world == 1:
+            assert np.array_equal(last.word_ids, csr.word_ids), "e2e and staged results differ"
+        h2d = int(w.qblob.nbytes + w.qoffs.nbytes)
+        n_match = int(last[1].size) if world > 1 and last is not None else int(csr.offsets[-1])
+        d2h = int(8 * (w.nq + 1) + 4 * n_match + (8 * 5 * w.nq if world == 1 else 0))
+        e2e = {"value": logical_pairs_all * args.steps / e2e_s, "unit": "comparisons/s",
+               "h2d_bytes_per_step": h2d * (world if world > 1 else 1), "d2h_bytes_per_step": d2h,
+               "ms_per_step": 1e3 * e2e_s / args.steps,
+               "gather_ms_per_step": statistics.mean(gather[-args.steps:]) if gather else None,
+               "gather": ("host: libfpg.so concatenates the shard rows (fpg_batch_download)" if world == 1 else
+                          "device: NCCL p2p of the ranks' CSRs to rank 0 + fpg_csr_merge_device, one D2H"),
+               "l2": L2_NOTE}
 
     if rank != 0:
         return
-    # roofline of the dominant kernel (K2): the pairs it evaluated per launch
-    # (length-compatible pairs minus those skipped by the weight window) / the
-    # launch's CUDA-event time, against the ALU-pipe bound of the bit-sliced
-    # test (DESIGN.md section 3)
-    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    sms = torch.cuda.get_device_properties(dev0).multi_processor_count
     sm_mhz = clk.get("sm_max_mhz") or 1965.0
-    filt_avg_ms = statistics.mean(filt_ms)
-    achieved = (scanned or executed) / (filt_avg_ms / 1e3) / 1e12
+    # roofline of the dominant kernel (K2) on shard 0: the pairs it evaluated
+    # per launch (length-compatible pairs minus those the weight window
+    # skipped; DESIGN.md section 3) / the launch's CUDA-event time, against
+    # the ALU-pipe bound of the bit-sliced test
+    t0s = t_last[0]
+    filt_avg_ms = statistics.mean(f[0] for f in filt_ms)
+    achieved = t0s["scanned_pairs"] / (filt_avg_ms / 1e3) / 1e12
     shape = d.scan_shape()
-    ops = ops_per_comparison(scheme, shape["sig_fields"])
-    popc_peak = sms * sm_mhz * 1e6 * POPC_PER_CLK_PER_SM / math.ceil(scheme.width() / 32) / 1e12
+    ops = ops_per_comparison(w.scheme, shape["sig_fields"])
+    lop3_clk, lop3_basis = alu_peak()
+    popc_peak = sms * sm_mhz * 1e6 * POPC_PER_CLK_PER_SM / math.ceil(w.scheme.width() / 32) / 1e12
     if shape["sliced"]:
-        peak = sms * sm_mhz * 1e6 * ALU_PER_CLK_PER_SM / ops / 1e12
-        bound, basis = "int-alu", (f"{sms} SMs x {sm_mhz:.0f} MHz x {ALU_PER_CLK_PER_SM} LOP3/clk/SM / "
+        peak = sms * sm_mhz * 1e6 * lop3_clk / ops / 1e12
+        bound, basis = "int-alu", (f"{sms} SMs x {sm_mhz:.0f} MHz x {lop3_clk:.1f} LOP3/clk/SM ({lop3_basis}) / "
                                    f"{ops:.3f} LOP3 per comparison (bit-sliced test, {shape['sig_fields']} sig' planes)")
     else:
         peak = popc_peak
         bound, basis = "int-xu", f"{sms} SMs x {sm_mhz:.0f} MHz x {POPC_PER_CLK_PER_SM} POPC/clk/SM / ceil(W/32)"
-    traffic = profiled_traffic(f"config{args.config}", _cell_name(args.config, args.cell))
+    traffic = profiled_traffic(f"config{args.config}", w.cell_name())
     line = {
-        "metric": "k=1 query x word comparisons/s (logical Q*N)",
-        "value": value, "unit": "comparisons/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "metric": METRIC, "value": value, "unit": "comparisons/s", "n_gpus": n_gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if w.strong else "weak", "vs_baseline": None,
         "dtype": "u8", "data": f"synthetic (seeded generator, config {args.config}; see corpus.py)",
-        "config": {"workload": f"config{args.config}", "cell": _cell_name(args.config, args.cell),
-                   "n_words_per_gpu": n, "n_queries": nq, "length_prefilter": True, "query_stats": True,
-                   "l2": "flushed between steps (256 MB write)" if flush is not None else "not flushed",
-                   "parallelism": f"dict-shard x{world}"},
-        "queries_per_s": nq * args.steps / (total_ms / 1e3),
-        "executed_pairs_per_step": executed, "evaluated_pairs_per_step": scanned, "survivors_per_step": survivors,
-        "verifier_candidates_per_step": candidates,
-        "matches_per_step": int(csr.offsets[-1]),
-        "construction_s": build_s,
+        "config": w.config(n_gpus),
+        "queries_per_s": w.nq * args.steps / (total_ms / 1e3),
+        "executed_pairs_per_step": sum(t["executed_pairs"] for t in t_last),
+        "evaluated_pairs_per_step": sum(t["scanned_pairs"] for t in t_last),
+        "survivors_per_step": sum(t["survivors"] for t in t_last),
+        "verifier_candidates_per_step": sum(t["candidates"] for t in t_last),
+        "matches_per_step": int(csr.offsets[-1]) if world == 1 else None,
+        "shard_ms_per_step": [statistics.mean(s[i] for s in shard_ms) for i in range(nsh)],
+        "construction_s": build_s, "setup_s": w.setup_s,
         "gpu_launches": launches,
-        "e2e": {"value": e2e_value, "unit": "comparisons/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "l2": "flushed between steps"},
+        "e2e": e2e,
         "roofline": {"bound": bound, "kernel": "k_slice (K2 filter+verify)" if shape["sliced"] else "k_scan (K2)",
                      "achieved": achieved, "peak": peak, "unit": "Tcmp/s", "frac": achieved / peak,
+                     "pairs_basis": "pairs K2 evaluated (length-compatible minus weight-window skips)",
                      "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",
                      "peak_basis": basis,
                      "popc_equiv_peak": popc_peak, "popc_equiv_frac": achieved / popc_peak,
                      "filter_ms_per_launch": filt_avg_ms, "filter_share_of_step": filt_avg_ms / ms_per_step},
         "clocks": clk,
     }
-    if not args.no_cpu_baseline:
-        rate, kind, sample, dt = cpu_reference_rate(blob, offs, qblob, qoffs, scheme, metric,
-                                                    args.cpu_seconds, host_threads())
-        line["cpu_baseline"] = {"value": rate, "unit": "comparisons/s", "cores": host_threads(), "kind": kind,
+    if not args.no_cpu_baseline and n_gpus == 1:
+        rate, kind = cpu_reference_rate(w, args.cpu_seconds, host_threads())
+        r, sample = rate(args.cpu_seconds)
+        line["cpu_baseline"] = {"value": r, "unit": "comparisons/s", "cores": host_threads(), "kind": kind,
                                 "sample": sample}
     print(json.dumps(line), flush=True)
 
 
-def _cell_name(cfg, cell):
-    from paper_1711_08475_b200.corpus import CELLS
+def _gather_merge(batch, h_out):
+    """One process per GPU: this rank's device CSR to rank 0 over NCCL, merged
+    there on the GPU and copied to the host (sharding.query_batch_distributed
+    without the run, which the caller already timed)."""
+    import torch
+    import torch.distributed as dist
 
-    v, w, b, p, m = CELLS[cfg][cell]
-    extra = f" b={b}" if v.name == "Count" else (f" p={p}" if v.name == "Position" else "")
-    return f"{v.name}-{w}{extra} {m.name} k=1"
+    from paper_1711_08475_b200.sharding import device_tensors, gather_rows, merge_device
+
+    csr = batch.device_csr(0)
+    off, ids = device_tensors(csr)
+    parts = gather_rows(off, ids, dst=0)
+    if dist.get_rank() != 0:
+        return None
+    m_off, m_ids = merge_device(parts, csr["nq"], csr["device"])
+    h_off, h_ids = h_out[0][: m_off.numel()], h_out[1][: m_ids.numel()]
+    h_off.copy_(m_off, non_blocking=True)
+    h_ids.copy_(m_ids, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return h_off.numpy().view(np.uint64), h_ids.numpy().view(np.uint32)
 
 
 if __name__ == "__main__":

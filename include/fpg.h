@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define FPG_ABI_VERSION 2
+#define FPG_ABI_VERSION 3
 
 /* status codes */
 #define FPG_OK 0
@@ -156,6 +156,31 @@ int fpg_batch_download(fpg_batch* batch, fpg_result* out);
 int fpg_batch_last_timing(const fpg_batch* batch, int32_t shard, double* run_ms,
                           double* filter_ms, uint64_t* executed_pairs, uint64_t* survivors,
                           uint64_t* kernel_launches);
+
+/* Host-side milliseconds of the batch's last upload (length bucketing +
+ * H2D), last download (D2H wait) and last result assembly (the host gather
+ * of shard rows into one CSR + QueryStats). */
+int fpg_batch_last_host_ms(const fpg_batch* batch, double* upload_ms, double* download_ms,
+                           double* assemble_ms);
+
+/* Device-resident result of the last successful run on `shard`: the shard's
+ * CSR (nq + 1 offsets, *total word ids, global input-order ids, ascending
+ * per query) in the memory of *device.  Valid until the batch's next run or
+ * destruction.  For device-side gathers across processes (one process per
+ * GPU): see fpg_csr_merge_device. */
+int fpg_batch_device_csr(const fpg_batch* batch, int32_t shard, int32_t* device, uint64_t* total,
+                         const uint64_t** d_offsets, const uint32_t** d_ids);
+
+/* Device-side gather of per-shard CSRs (all in `device` memory, e.g. after an
+ * NVLink/NCCL transfer) into one CSR in shard order: row q of the result is
+ * row q of part 0, then of part 1, ...  That is the oracle's order when
+ * part i holds the ids of shard i (contiguous, ascending id ranges).
+ * d_out_offsets: nq + 1; d_out_ids: the sum of the parts' totals.
+ * `stream` is a cudaStream_t (NULL = legacy default stream); the call is
+ * asynchronous on it.  1 <= nparts <= 16. */
+int fpg_csr_merge_device(int32_t device, int32_t nparts, const uint64_t* const* d_offsets,
+                         const uint32_t* const* d_ids, uint64_t nq, uint64_t* d_out_offsets,
+                         uint32_t* d_out_ids, void* stream);
 
 /* Shape of the dictionary's K2 path: *sliced = 1 for the bit-sliced k_slice
  * (0: generic per-pair k_scan), *sig_fields = S extra sig' planes. */

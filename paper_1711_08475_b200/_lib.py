@@ -91,12 +91,20 @@ FPG_SIGNATURES = {
                                              c_u64p]),
     "fpg_batch_last_candidates": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, c_u64p]),
     "fpg_batch_last_scanned": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, c_u64p]),
+    "fpg_batch_last_host_ms": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
+                                              ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+    "fpg_batch_device_csr": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                                            c_u64p, ctypes.POINTER(ctypes.c_void_p),
+                                            ctypes.POINTER(ctypes.c_void_p)]),
+    "fpg_csr_merge_device": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p),
+                                            ctypes.POINTER(ctypes.c_void_p), ctypes.c_uint64, ctypes.c_void_p,
+                                            ctypes.c_void_p, ctypes.c_void_p]),
     "fpg_dict_scan_shape": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32),
                                            ctypes.POINTER(ctypes.c_int32)]),
 }
 
 FPG_OK, FPG_EINVAL, FPG_EUNSUPPORTED, FPG_ECUDA, FPG_ENOMEM = 0, -1, -2, -3, -4
-FPG_ABI_VERSION = 2  # include/fpg.h
+FPG_ABI_VERSION = 3  # include/fpg.h
 
 _fpg = None
 _corpus = None

@@ -17,7 +17,7 @@ CSRC = PKG / "csrc"
 LIB = PKG / "lib"
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-warn-spills"]
+              "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills"]
 
 
 def _nvcc() -> str:
@@ -35,14 +35,24 @@ def _stale(target: Path, sources) -> bool:
 
 
 def build_fpg(force: bool = False) -> Path:
+    """Every csrc/*.cu compiled to an object in parallel (the K2 template
+    instantiations live in their own translation units), then linked."""
     LIB.mkdir(exist_ok=True)
     out = LIB / "libfpg.so"
-    srcs = sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "fpg.h"]
+    units = sorted(CSRC.glob("*.cu"))
+    srcs = units + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [ROOT / "include" / "fpg.h"]
     if force or _stale(out, srcs):
-        tmp = out.with_suffix(".so.tmp")
+        obj_dir = LIB / "obj"
+        obj_dir.mkdir(exist_ok=True)
         dbg = ["-DFPG_DEBUG"] if os.environ.get("FPG_DEBUG") == "1" else []
-        cmd = [_nvcc(), *NVCC_FLAGS, *dbg, "-o", str(tmp), str(CSRC / "fpg_api.cu")]
-        subprocess.run(cmd, check=True)
+        objs = [obj_dir / (u.stem + ".o") for u in units]
+        procs = [subprocess.Popen([_nvcc(), *NVCC_FLAGS, *dbg, "-c", "-o", str(o), str(u)])
+                 for u, o in zip(units, objs)]
+        if any(pr.wait() != 0 for pr in procs):
+            raise subprocess.CalledProcessError(1, "nvcc (see output above)")
+        tmp = out.with_suffix(".so.tmp")
+        subprocess.run([_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp),
+                        *map(str, objs)], check=True)
         os.replace(tmp, out)
     return out
 

@@ -31,24 +31,13 @@
 #include <thrust/iterator/counting_iterator.h>
 
 #include "../../include/fpg.h"
+#include "fpg_host.h"
 #include "fpg_kernels.cuh"
 
 namespace {
 
 thread_local std::string g_last_error;
-
-struct Error : std::runtime_error {
-    int code;
-    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
-};
-
-#define CK(x)                                                                                  \
-    do {                                                                                       \
-        cudaError_t e_ = (x);                                                                  \
-        if (e_ != cudaSuccess)                                                                 \
-            throw Error(FPG_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_) + " (" +    \
-                                       __FILE__ + ":" + std::to_string(__LINE__) + ")");       \
-    } while (0)
+using fpg_host::Error;
 
 template <class F>
 int guarded(F&& f) {
@@ -445,6 +434,7 @@ struct fpg_dict {
     double build_seconds = 0;
     std::mutex cache_mu;              // guards `pool`
     std::vector<fpg_batch*> pool;     // idle scratch batches of fpg_query_batch (one per concurrent caller)
+    std::atomic<int> live_batches{0}; // fpg_batch_create handles not yet destroyed (they use the shards)
     ~fpg_dict();
 };
 
@@ -496,7 +486,10 @@ struct fpg_batch {
     HBuf<uint64_t> h_bbase;
     std::vector<std::unique_ptr<ShardBatch>> sb;
     fpg_query_options opt{};
-    bool ran = false;
+    bool uploaded = false;  // a batch of queries is on the devices
+    bool ran = false;       // the last run succeeded (download is valid)
+    bool external = false;  // created by fpg_batch_create (counted in dict->live_batches)
+    double upload_ms = 0, download_ms = 0, assemble_ms = 0;  // host-side times of the last calls
     ~fpg_batch() {
         for (auto& s : sb) {
             cudaSetDevice(s->sh->device);
@@ -559,32 +552,6 @@ void for_each_shard(size_t n, F&& f) {
         if (codes[i]) throw Error(codes[i], "shard " + std::to_string(i) + ": " + errs[i]);
 }
 
-template <int KIND, int W, bool STATS>
-void launch_scan(const fpg::Tile* tiles, uint32_t ntiles, const fpg::ScanParams& P, cudaStream_t st,
-                 int device) {
-    auto kern = fpg::k_scan<KIND, W, STATS>;
-    constexpr size_t smem = fpg::scan_smem_bytes(W, STATS);
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, fpg::kScanThreads, smem));
-    const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)sms * std::max(per_sm, 1) * 8);
-    kern<<<(unsigned)std::max<uint64_t>(grid, 1), fpg::kScanThreads, smem, st>>>(tiles, ntiles, P);
-    CK(cudaGetLastError());
-}
-
-template <int KIND>
-void launch_w(int width, bool stats, const fpg::Tile* tiles, uint32_t ntiles, const fpg::ScanParams& P,
-              cudaStream_t st, int device) {
-    if (width == 16) stats ? launch_scan<KIND, 16, true>(tiles, ntiles, P, st, device)
-                           : launch_scan<KIND, 16, false>(tiles, ntiles, P, st, device);
-    else if (width == 32) stats ? launch_scan<KIND, 32, true>(tiles, ntiles, P, st, device)
-                                : launch_scan<KIND, 32, false>(tiles, ntiles, P, st, device);
-    else stats ? launch_scan<KIND, 64, true>(tiles, ntiles, P, st, device)
-               : launch_scan<KIND, 64, false>(tiles, ntiles, P, st, device);
-}
-
 // Distance form per scheme: plain popcount (occurrence, halved, one-hot
 // count-16), compile-time folds for count b=2/4 and position p=3, else the
 // generic runtime fold.
@@ -596,43 +563,7 @@ int dist_kind(const fpg::SchemeParams& S, bool onehot) {
 
 void dispatch_scan(const fpg::SchemeParams& S, bool onehot, bool stats, const fpg::Tile* tiles, uint32_t ntiles,
                    const fpg::ScanParams& P, cudaStream_t st, int device) {
-    switch (dist_kind(S, onehot)) {
-        case fpg::kPopc: launch_w<fpg::kPopc>(S.width, stats, tiles, ntiles, P, st, device); break;
-        case fpg::kFold2: launch_w<fpg::kFold2>(S.width, stats, tiles, ntiles, P, st, device); break;
-        case fpg::kFold4: launch_w<fpg::kFold4>(S.width, stats, tiles, ntiles, P, st, device); break;
-        case fpg::kPos3: launch_w<fpg::kPos3>(S.width, stats, tiles, ntiles, P, st, device); break;
-        default: launch_w<fpg::kGeneric>(S.width, stats, tiles, ntiles, P, st, device); break;
-    }
-}
-
-template <int NP, int FW, int EXTRA, int S>
-void launch_slice(const fpg::SliceTile* tiles, uint32_t ntiles, const fpg::SliceParams& P, cudaStream_t st,
-                  int device) {
-    auto kern = fpg::k_slice<NP, FW, EXTRA, S>;
-    constexpr size_t smem = fpg::slice_smem_bytes(NP + S);
-    static int resident[64] = {0};  // per device: CTAs resident on the whole GPU (0 = not yet queried)
-    const int dv = device & 63;
-    if (!resident[dv]) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int sms = 148, per_sm = 0;
-        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, fpg::kSliceThreads, smem));
-        resident[dv] = sms * std::max(per_sm, 1);
-    }
-    const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)resident[dv]);
-    kern<<<(unsigned)std::max<uint64_t>(grid, 1), fpg::kSliceThreads, smem, st>>>(tiles, ntiles, P);
-    CK(cudaGetLastError());
-}
-
-template <int NP, int FW, int EXTRA>
-void launch_slice_s(int nsig, const fpg::SliceTile* tiles, uint32_t ntiles, const fpg::SliceParams& P,
-                    cudaStream_t st, int device) {
-    switch (nsig) {
-        case 0: launch_slice<NP, FW, EXTRA, 0>(tiles, ntiles, P, st, device); break;
-        case 8: launch_slice<NP, FW, EXTRA, 8>(tiles, ntiles, P, st, device); break;
-        case 12: launch_slice<NP, FW, EXTRA, 12>(tiles, ntiles, P, st, device); break;
-        default: launch_slice<NP, FW, EXTRA, 16>(tiles, ntiles, P, st, device); break;
-    }
+    fpg_host::dispatch_scan(dist_kind(S, onehot), S.width, stats, tiles, ntiles, P, st, device);
 }
 
 // Field width of the scheme's multi-bit fields (1 for occurrence / halved).
@@ -647,23 +578,12 @@ bool slice_supported(const fpg_scheme& s) {
     return fw >= 1 && fw <= 4;
 }
 
-template <int NP>
-void dispatch_slice_w(int fw, int nsig, const fpg::SliceTile* tiles, uint32_t ntiles, const fpg::SliceParams& P,
-                      cudaStream_t st, int device) {
-    switch (fw) {
-        case 1: launch_slice_s<NP, 1, 0>(nsig, tiles, ntiles, P, st, device); break;
-        case 2: launch_slice_s<NP, 2, 0>(nsig, tiles, ntiles, P, st, device); break;
-        case 3: launch_slice_s<NP, 3, NP % 3>(nsig, tiles, ntiles, P, st, device); break;
-        default: launch_slice_s<NP, 4, 0>(nsig, tiles, ntiles, P, st, device); break;
-    }
-}
-
 void dispatch_slice(const fpg_scheme& sc, int nsig, const fpg::SliceTile* tiles, uint32_t ntiles,
                     const fpg::SliceParams& P, cudaStream_t st, int device) {
     const int fw = field_width_of(sc);
-    if (sc.width == 16) dispatch_slice_w<16>(fw, nsig, tiles, ntiles, P, st, device);
-    else if (sc.width == 32) dispatch_slice_w<32>(fw, nsig, tiles, ntiles, P, st, device);
-    else dispatch_slice_w<64>(fw, nsig, tiles, ntiles, P, st, device);
+    if (sc.width == 16) fpg_host::dispatch_slice_16(fw, nsig, tiles, ntiles, P, st, device);
+    else if (sc.width == 32) fpg_host::dispatch_slice_32(fw, nsig, tiles, ntiles, P, st, device);
+    else fpg_host::dispatch_slice_64(fw, nsig, tiles, ntiles, P, st, device);
 }
 
 bool compatible(int metric, int k, int lq, int lw) {
@@ -932,11 +852,13 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         // scattered into their query's segment, then each segment sorted by
         // one warp (<= kSegMax matches).  Batches known to have larger
         // segments skip the warp sort; the host sorts their segments below.
-        if (nq) {
+        if (nq) {  // accumulated in 64 bits: a batch may hold >= 2^32 matches
             size_t tmp = 0;
-            CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, S.qsurv.p + nq, S.offsets.p, (int)nq, st));
+            CK(cub::DeviceScan::ExclusiveScan(nullptr, tmp, S.qsurv.p + nq, S.offsets.p, cuda::std::plus<>{}, uint64_t(0),
+                                              (int)nq, st));
             S.cub_tmp.reserve(tmp);
-            CK(cub::DeviceScan::ExclusiveSum(S.cub_tmp.p, tmp, S.qsurv.p + nq, S.offsets.p, (int)nq, st));
+            CK(cub::DeviceScan::ExclusiveScan(S.cub_tmp.p, tmp, S.qsurv.p + nq, S.offsets.p, cuda::std::plus<>{}, uint64_t(0),
+                                              (int)nq, st));
         }
         fpg::k_seg_scatter<<<kScatterBlocks, 256, 0, st>>>(S.out.p, S.counters.p, S.counters.p + 5, S.out.cap,
                                                            S.offsets.p, S.qsurv.p + nq, S.ids.p, S.offsets.p + nq,
@@ -965,6 +887,7 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         // segmented sort of the 32-bit word ids; later runs of this batch
         // skip the warp sort)
         S.seg_k4 = false;
+        if (S.total >= (1ull << 31)) throw Error(FPG_EINVAL, "more than 2^31 - 1 matches in one shard's batch");
         S.ids2.reserve(S.total);
         size_t tmp = 0;
         CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, S.ids.p, S.ids2.p, (int)S.total, (int)nq, S.offsets.p,
@@ -1106,6 +1029,8 @@ void upload(fpg_batch* B, const uint8_t* qbytes, const uint64_t* qoffsets, uint6
         }
         if (sync) CK(cudaStreamSynchronize(st));  // caller buffers may be reused once upload returns
     });
+    B->uploaded = true;
+    B->upload_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (g_trace) {
         const auto t2 = std::chrono::steady_clock::now();
         std::fprintf(stderr, "fpg upload: host bucketing %.1f us, h2d %.1f us\n",
@@ -1116,6 +1041,8 @@ void upload(fpg_batch* B, const uint8_t* qbytes, const uint64_t* qoffsets, uint6
 
 void run(fpg_batch* B, const fpg_query_options* o) {
     check_opts(B->dict, o);
+    if (!B->uploaded) throw Error(FPG_EINVAL, "fpg_batch_run before fpg_batch_upload");
+    B->ran = false;  // stays false if a shard fails: download refuses stale results
     B->opt = *o;
     for_each_shard(B->sb.size(), [&](size_t i) { run_shard(B->dict, B, *B->sb[i], *o); });
     B->ran = true;
@@ -1129,6 +1056,7 @@ void download(fpg_batch* B, fpg_result* out) {
     const auto t0 = std::chrono::steady_clock::now();
     for_each_shard(B->sb.size(), [&](size_t i) { download_shard(B, *B->sb[i], stats); });
     const auto t1 = std::chrono::steady_clock::now();
+    B->download_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
     const uint64_t nq = B->nq;
     std::memset(out, 0, sizeof(*out));
     out->nq = nq;
@@ -1198,6 +1126,7 @@ void download(fpg_batch* B, fpg_result* out) {
             }
         });
     }
+    B->assemble_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count();
     if (g_trace) {
         const auto t2 = std::chrono::steady_clock::now();
         std::fprintf(stderr, "fpg download: d2h %.1f us, assemble %.1f us\n",
@@ -1311,6 +1240,8 @@ void assign_ranges(fpg_dict& D, uint64_t n) {
     for (size_t g = 0; g < G; ++g) {
         D.shards[g]->base = n * g / G;
         D.shards[g]->n = n * (g + 1) / G - D.shards[g]->base;
+        // the shard's CUB sorts index with int
+        if (D.shards[g]->n >= (1ull << 31)) throw Error(FPG_EINVAL, "more than 2^31 - 1 words in one shard");
     }
 }
 
@@ -1486,7 +1417,11 @@ int fpg_byte_histogram(const uint8_t* bytes, uint64_t nbytes, int32_t device, ui
 }
 
 int fpg_dict_destroy(fpg_dict* dict) {
-    return guarded([&] { delete dict; });
+    return guarded([&] {
+        if (dict && dict->live_batches.load() > 0)
+            throw Error(FPG_EINVAL, "fpg_dict_destroy with live batches: destroy them first");
+        delete dict;
+    });
 }
 
 int fpg_dict_size(const fpg_dict* dict, uint64_t* n) {
@@ -1563,11 +1498,16 @@ int fpg_batch_create(fpg_dict* dict, fpg_batch** out) {
     return guarded([&] {
         if (!dict || !out) throw Error(FPG_EINVAL, "null argument");
         make_batch(dict, out);
+        (*out)->external = true;
+        ++dict->live_batches;
     });
 }
 
 int fpg_batch_destroy(fpg_batch* batch) {
-    return guarded([&] { delete batch; });
+    return guarded([&] {
+        if (batch && batch->external) --batch->dict->live_batches;
+        delete batch;
+    });
 }
 
 int fpg_batch_upload(fpg_batch* batch, const uint8_t* qbytes, const uint64_t* qoffsets, uint64_t nq) {
@@ -1602,6 +1542,65 @@ int fpg_batch_last_timing(const fpg_batch* batch, int32_t shard, double* run_ms,
         if (executed_pairs) *executed_pairs = S.executed;
         if (survivors) *survivors = S.survivors;
         if (kernel_launches) *kernel_launches = S.launches;
+    });
+}
+
+int fpg_batch_last_host_ms(const fpg_batch* batch, double* upload_ms, double* download_ms, double* assemble_ms) {
+    return guarded([&] {
+        if (!batch) throw Error(FPG_EINVAL, "null batch");
+        if (upload_ms) *upload_ms = batch->upload_ms;
+        if (download_ms) *download_ms = batch->download_ms;
+        if (assemble_ms) *assemble_ms = batch->assemble_ms;
+    });
+}
+
+int fpg_batch_device_csr(const fpg_batch* batch, int32_t shard, int32_t* device, uint64_t* total,
+                         const uint64_t** d_offsets, const uint32_t** d_ids) {
+    return guarded([&] {
+        if (!batch || shard < 0 || (size_t)shard >= batch->sb.size()) throw Error(FPG_EINVAL, "bad shard");
+        if (!batch->ran) throw Error(FPG_EINVAL, "fpg_batch_device_csr before a successful fpg_batch_run");
+        const ShardBatch& S = *batch->sb[(size_t)shard];
+        if (device) *device = S.sh->device;
+        if (total) *total = S.total;
+        if (d_offsets) *d_offsets = S.offsets.p;
+        if (d_ids) *d_ids = S.ids_out;
+    });
+}
+
+int fpg_csr_merge_device(int32_t device, int32_t nparts, const uint64_t* const* d_offsets,
+                         const uint32_t* const* d_ids, uint64_t nq, uint64_t* d_out_offsets, uint32_t* d_out_ids,
+                         void* stream) {
+    return guarded([&] {
+        if (nparts < 1 || nparts > fpg::kMaxMergeParts) throw Error(FPG_EINVAL, "nparts out of range");
+        if (!d_offsets || !d_ids || !d_out_offsets) throw Error(FPG_EINVAL, "null argument");
+        CK(cudaSetDevice(device));
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        fpg::MergeParts mp{};
+        mp.n = nparts;
+        for (int i = 0; i < nparts; ++i) {
+            if (!d_offsets[i]) throw Error(FPG_EINVAL, "null part offsets");
+            mp.off[i] = d_offsets[i];
+            mp.ids[i] = d_ids[i];
+        }
+        // row lengths summed over the parts (+ a zero at nq), then their
+        // exclusive scan: the merged offsets
+        size_t tmp = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, d_out_offsets, d_out_offsets, nq + 1, st));
+        const size_t cnt_bytes = ((nq + 1) * sizeof(uint64_t) + 255) & ~size_t(255);
+        uint8_t* d_tmp = nullptr;
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&d_tmp), cnt_bytes + std::max<size_t>(tmp, 1), st));
+        uint64_t* d_cnt = reinterpret_cast<uint64_t*>(d_tmp);
+        const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(cdiv(nq + 1, 256), 148 * 16));
+        fpg::k_merge_counts<<<blocks, 256, 0, st>>>(mp, nq, d_cnt);
+        CK(cudaGetLastError());
+        CK(cub::DeviceScan::ExclusiveSum(d_tmp + cnt_bytes, tmp, d_cnt, d_out_offsets, nq + 1, st));
+        CK(cudaFreeAsync(d_tmp, st));
+        if (nq) {
+            fpg::k_merge_rows<<<(unsigned)std::min<uint64_t>(cdiv(nq * 32, 256), 148 * 16), 256, 0, st>>>(
+                mp, nq, d_out_offsets, d_out_ids);
+            CK(cudaGetLastError());
+        }
+        g_launches += 4;
     });
 }
 

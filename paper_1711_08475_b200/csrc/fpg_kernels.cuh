@@ -281,6 +281,7 @@ __global__ void __launch_bounds__(256) k_build(const uint8_t* __restrict__ blob,
 // Lengths, identity ids and the length histogram (lengths < 256 counted in
 // shared memory first: a dictionary has few distinct lengths, and global
 // atomics on them would serialise).  blockDim == 256.
+#ifndef FPG_K2_TU  // defined once, in fpg_api.cu
 __global__ void k_lengths(const uint64_t* __restrict__ offsets, uint64_t n,
                           uint16_t* __restrict__ len_out, uint32_t* __restrict__ idx_out,
                           uint32_t* __restrict__ hist, uint32_t* __restrict__ too_long) {
@@ -302,12 +303,15 @@ __global__ void k_lengths(const uint64_t* __restrict__ offsets, uint64_t n,
     __syncthreads();
     if (h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
 }
+#endif
 
+#ifndef FPG_K2_TU  // defined once, in fpg_api.cu
 __global__ void k_scatter_prints(const uint64_t* __restrict__ fp, const uint32_t* __restrict__ ids,
                                  uint64_t n, uint64_t* __restrict__ out) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[ids[i]] = fp[i];
 }
+#endif
 
 // ---------------------------------------------------------------- K4 CSR
 constexpr uint32_t kSegMax = 32;  // K4 warp-sorts segments up to this size
@@ -371,6 +375,7 @@ __device__ __forceinline__ bool match_run_head(bool hit, uint32_t qid, uint32_t 
 }
 
 // K4 segmented (all segments <= kSegMax): keys -> their query's segment.
+#ifndef FPG_K2_TU  // defined once, in fpg_api.cu
 __global__ void k_seg_scatter(const unsigned long long* __restrict__ keys, const unsigned long long* __restrict__ slots,
                               const unsigned long long* __restrict__ matches, uint64_t cap,
                               const uint64_t* __restrict__ offsets_in, uint32_t* __restrict__ cursor,
@@ -401,8 +406,10 @@ __global__ void k_seg_scatter(const unsigned long long* __restrict__ keys, const
         if (pos < cap) ids[pos] = (uint32_t)(id_base + __ldg(w_ids + (uint32_t)k));
     }
 }
+#endif
 
 // One warp per query: bitonic sort of its <= 32 word ids in registers.
+#ifndef FPG_K2_TU  // defined once, in fpg_api.cu
 __global__ void k_seg_sort(const uint64_t* __restrict__ offsets, uint64_t nq, uint64_t cap, uint32_t* __restrict__ ids,
                            unsigned long long* __restrict__ big_seg) {
     const uint64_t q = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -430,6 +437,47 @@ __global__ void k_seg_sort(const uint64_t* __restrict__ offsets, uint64_t nq, ui
     }
     if (lane < n) ids[o + lane] = v;
 }
+#endif
+
+// ---------------------------------------------------------------- CSR merge
+// Shards own ascending, contiguous input-order id ranges, so the global
+// (query asc, word asc) CSR is each query's part rows concatenated in part
+// order: a gather, not a sort.
+constexpr int kMaxMergeParts = 16;
+struct MergeParts {
+    int n;
+    const uint64_t* off[kMaxMergeParts];  // nq + 1 offsets per part
+    const uint32_t* ids[kMaxMergeParts];
+};
+
+// cnt[q] = sum over parts of row q's length, cnt[nq] = 0 (the scan's total).
+#ifndef FPG_K2_TU  // defined once, in fpg_api.cu
+__global__ void k_merge_counts(const __grid_constant__ MergeParts mp, uint64_t nq, uint64_t* __restrict__ cnt) {
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q <= nq; q += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t c = 0;
+        if (q < nq)
+            for (int p = 0; p < mp.n; ++p) c += __ldg(mp.off[p] + q + 1) - __ldg(mp.off[p] + q);
+        cnt[q] = c;
+    }
+}
+#endif
+
+// One warp per query: its part rows, in part order, to the merged row.
+#ifndef FPG_K2_TU  // defined once, in fpg_api.cu
+__global__ void k_merge_rows(const __grid_constant__ MergeParts mp, uint64_t nq, const uint64_t* __restrict__ out_off,
+                             uint32_t* __restrict__ out_ids) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = (uint64_t)gridDim.x * blockDim.x / 32;
+    for (uint64_t q = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; q < nq; q += warps) {
+        uint64_t at = out_off[q];
+        for (int p = 0; p < mp.n; ++p) {
+            const uint64_t a = __ldg(mp.off[p] + q), b = __ldg(mp.off[p] + q + 1);
+            for (uint64_t i = a + lane; i < b; i += 32) out_ids[at + (i - a)] = __ldg(mp.ids[p] + i);
+            at += b - a;
+        }
+    }
+}
+#endif
 
 }  // namespace fpg
 

@@ -161,7 +161,7 @@ __device__ __forceinline__ bool hamming_le(const uint8_t* a, const uint8_t* b, i
 // levenshtein_bounded (edit_distance.hpp:31-64) as a test: the 2k+1-wide
 // band of the DP, cell (i, j) at band index t = j - i + k, early exit when a
 // row's minimum exceeds k.
-__device__ __noinline__ bool levenshtein_le(const uint8_t* s1, int m, const uint8_t* s2, int n, int k) {
+static __device__ __noinline__ bool levenshtein_le(const uint8_t* s1, int m, const uint8_t* s2, int n, int k) {
     if (m > n) {
         const uint8_t* ts = s1; s1 = s2; s2 = ts;
         const int tn = m; m = n; n = tn;

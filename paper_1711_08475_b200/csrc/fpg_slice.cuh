@@ -565,6 +565,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
 // ---------------------------------------------------------------- K1b planes
 // One warp per slab: lane i holds word 32 s + i of its bucket; plane b is the
 // ballot of bit b of the words' codes (fingerprint bits, then sig' bits).
+#ifndef FPG_K2_TU  // defined once, in fpg_api.cu
 __global__ void k_planes(const uint64_t* __restrict__ fp, const uint32_t* __restrict__ sigp,
                          const uint32_t* __restrict__ weight, uint2* __restrict__ slab_w,
                          const uint32_t* __restrict__ slab_start,  // per length: first global slab (L1 + 1)
@@ -612,8 +613,10 @@ __global__ void k_planes(const uint64_t* __restrict__ fp, const uint32_t* __rest
         if (b < npt) planes[plane_base[L] + (uint64_t)b * ns + s] = mine[r];
     }
 }
+#endif
 
 // 256-bin byte histogram of a blob (sig' symbol ranking).
+#ifndef FPG_K2_TU  // defined once, in fpg_api.cu
 __global__ void k_hist256(const uint8_t* __restrict__ blob, uint64_t n, unsigned long long* __restrict__ hist) {
     __shared__ unsigned int h[256];
     h[threadIdx.x] = 0;  // blockDim == 256
@@ -623,5 +626,6 @@ __global__ void k_hist256(const uint8_t* __restrict__ blob, uint64_t n, unsigned
     __syncthreads();
     if (h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], (unsigned long long)h[threadIdx.x]);
 }
+#endif
 
 }  // namespace fpg

@@ -15,6 +15,7 @@ has the reference's method set plus ``query_batch``.  Schemes gain a width
 from __future__ import annotations
 
 import ctypes
+import weakref
 from dataclasses import dataclass
 from enum import IntEnum
 from typing import Iterable, Sequence
@@ -161,6 +162,25 @@ def english_letter_frequencies() -> list[tuple[int, float]]:
 
 # ---------------------------------------------------------------- schemes
 
+def _letter_capacity(v: int, width: int, b: int, p: int) -> int:
+    """Letters a scheme holds (fingerprint.hpp:84-100 with 16 -> W), -1 if
+    the parameters are invalid."""
+    if width not in (16, 32, 64):
+        return -1
+    if v == Variant.Occurrence:
+        return width
+    if v == Variant.OccurrenceHalved:
+        return width // 2
+    if v == Variant.Count:
+        return -1 if b <= 0 or width % b else width // b
+    if v == Variant.Position:
+        if p <= 0 or p > width:
+            return -1
+        slots = width // p
+        return slots + (width - slots * p)
+    return -1
+
+
 class Scheme:
     """fingerprint.hpp:57-162 with the width W as a parameter."""
 
@@ -202,8 +222,10 @@ class Scheme:
 
     @staticmethod
     def letter_capacity(v: Variant, b: int = 2, p: int = 3, width: int = 16) -> int:
-        """fingerprint.hpp:84-100, 16 -> W."""
-        c = load_fpg().fpg_letter_capacity(int(v), int(width), int(b), int(p))
+        """fingerprint.hpp:84-100, 16 -> W.  Host arithmetic (the same rule as
+        fpg_letter_capacity in libfpg.so; tests/test_host.py checks they
+        agree), so building a Scheme never loads the CUDA library."""
+        c = _letter_capacity(int(v), int(width), int(b), int(p))
         if c < 0:
             if Variant(v) == Variant.Count:
                 raise ValueError(f"count scheme: bits per count must divide {width}")
@@ -422,6 +444,7 @@ class GpuFingerprintedDictionary:
                                         len(devices), id_base, ctypes.byref(h)))
         self._h = h
         self._batch = None
+        self._batches = weakref.WeakSet()  # live Batch objects: closed before the dictionary
 
     @classmethod
     def from_text(cls, text, scheme: Scheme, devices: Sequence[int] = (0,), id_base: int = 0):
@@ -443,6 +466,7 @@ class GpuFingerprintedDictionary:
                                                   id_base, ctypes.byref(h)))
         self._h = h
         self._batch = None
+        self._batches = weakref.WeakSet()
         n = ctypes.c_uint64()
         check(self._lib.fpg_dict_size(h, ctypes.byref(n)))
         self._n = n.value
@@ -452,6 +476,8 @@ class GpuFingerprintedDictionary:
         if getattr(self, "_batch", None):
             self._lib.fpg_batch_destroy(self._batch)
             self._batch = None
+        for b in list(getattr(self, "_batches", ())):  # the C ABI refuses to drop a dict with live batches
+            b.close()
         if getattr(self, "_h", None):
             self._lib.fpg_dict_destroy(self._h)
             self._h = None
@@ -527,7 +553,20 @@ class GpuFingerprintedDictionary:
 
     # staged API (device-resident measurement)
     def batch(self) -> "Batch":
-        return Batch(self)
+        b = Batch(self)
+        self._batches.add(b)
+        return b
+
+
+def csr_merge_device(device: int, parts, nq: int, out_offsets: int, out_ids: int, stream: int = 0) -> None:
+    """fpg_csr_merge_device: parts = [(offsets_ptr, ids_ptr), ...] of per-shard
+    CSRs in `device` memory (shard order), merged into the device buffers
+    out_offsets (nq + 1 uint64) and out_ids, asynchronously on `stream`."""
+    n = len(parts)
+    offs = (ctypes.c_void_p * n)(*[ctypes.c_void_p(o) for o, _ in parts])
+    ids = (ctypes.c_void_p * n)(*[ctypes.c_void_p(i) for _, i in parts])
+    check(load_fpg().fpg_csr_merge_device(device, n, offs, ids, nq, ctypes.c_void_p(out_offsets),
+                                          ctypes.c_void_p(out_ids), ctypes.c_void_p(stream)))
 
 
 class Batch:
@@ -564,6 +603,23 @@ class Batch:
         check(self._lib.fpg_batch_last_scanned(self._h, shard, ctypes.byref(scan)))
         return {"run_ms": run_ms.value, "filter_ms": filt_ms.value, "executed_pairs": ex.value,
                 "survivors": sv.value, "launches": ln.value, "candidates": cand.value, "scanned_pairs": scan.value}
+
+    def host_ms(self) -> dict:
+        """Host-side ms of the last upload, download (D2H wait) and result
+        assembly (the host gather of shard rows)."""
+        u, d, a = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        check(self._lib.fpg_batch_last_host_ms(self._h, ctypes.byref(u), ctypes.byref(d), ctypes.byref(a)))
+        return {"upload_ms": u.value, "download_ms": d.value, "assemble_ms": a.value}
+
+    def device_csr(self, shard: int = 0) -> dict:
+        """Device pointers of the last run's CSR on `shard` (global ids):
+        {device, nq, total, offsets, ids}; valid until the next run."""
+        dev, total = ctypes.c_int32(), ctypes.c_uint64()
+        off, ids = ctypes.c_void_p(), ctypes.c_void_p()
+        check(self._lib.fpg_batch_device_csr(self._h, shard, ctypes.byref(dev), ctypes.byref(total),
+                                             ctypes.byref(off), ctypes.byref(ids)))
+        return {"device": dev.value, "nq": len(self._qoffs) - 1, "total": total.value,
+                "offsets": off.value or 0, "ids": ids.value or 0}
 
     def close(self) -> None:
         if getattr(self, "_h", None):

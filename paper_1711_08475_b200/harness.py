@@ -170,16 +170,20 @@ def sample_queries(words: Sequence, n: int, max_errors: int = 0, error_probabili
 # ---------------------------------------------------------------- timing
 
 def _pass(batch, opt: QueryOptions, iterations: int):
-    """`iterations` GPU batches; returns (device ns, summed QueryStats, matches of one pass)."""
-    total_ns, stats, matches = 0.0, None, 0
-    for it in range(iterations):
-        batch.run(opt, want_stats=(it == 0))
+    """`iterations` timed GPU batches; returns (device ns, QueryStats of one
+    pass, matches of one pass).  Like run_pass (bench.hpp:80-90) every timed
+    batch collects QueryStats; an untimed batch with the same options comes
+    first, so the timed ones reuse its tile plan and the stats and matches
+    are read outside the timed region."""
+    batch.run(opt, want_stats=True)
+    csr, st = batch.download()
+    matches = int(csr.offsets[-1])
+    s = st.sum(axis=0) if len(st) else np.zeros(5, np.uint64)
+    stats = QueryStats(*(int(x) for x in s))
+    total_ns = 0.0
+    for _ in range(iterations):
+        batch.run(opt, want_stats=True)
         total_ns += batch.timing()["run_ms"] * 1e6
-        if it == 0:
-            csr, st = batch.download()
-            matches = int(csr.offsets[-1])
-            s = st.sum(axis=0) if len(st) else np.zeros(5, np.uint64)
-            stats = QueryStats(*(int(x) for x in s))
     return total_ns, stats, matches
 
 

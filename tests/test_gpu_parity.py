@@ -386,3 +386,64 @@ def test_full_size_configs_vs_oracle(oracle, cfg, cell, nsample):
         assert np.array_equal(csr.row(q), o_ids[int(o_off[j]):int(o_off[j + 1])]), f"query {q}"
         assert np.array_equal(st[q], o_st[j]), f"stats of query {q}"
     assert int(st[:, 4].sum()) == len(csr.word_ids)
+
+
+# ---------------------------------------------------------------- shard gathers
+
+def test_device_csr_merge_equals_host_gather():
+    """fpg_csr_merge_device over the shards' device-resident CSRs (the
+    one-process-per-GPU gather, here with 3 shards on one GPU) equals the
+    host gather of fpg_batch_download, and lifecycle errors are reported."""
+    import torch
+
+    from paper_1711_08475_b200.sharding import device_tensors, merge_device
+
+    blob, offs, qblob, qoffs = _cfg_inputs(5, 60_000, 300)
+    s = make_scheme(blob, Variant.Occurrence, 16)
+    opt = QueryOptions(Metric.Levenshtein, 1, True, True)
+    with GpuFingerprintedDictionary((blob, offs), s, devices=(0, 0, 0)) as d:
+        b = d.batch()
+        with pytest.raises(ValueError):  # run before upload: FPG_EINVAL, not a crash
+            b.run(opt)
+        with pytest.raises(ValueError):
+            b.device_csr(0)
+        b.upload(qblob, qoffs)
+        b.run(opt, want_stats=True)
+        host, _ = b.download()
+        parts = [device_tensors(b.device_csr(i)) for i in range(3)]
+        assert sum(int(p[1].numel()) for p in parts) == len(host.word_ids)
+        m_off, m_ids = merge_device(parts, len(qoffs) - 1, 0)
+        torch.cuda.synchronize()
+        assert np.array_equal(m_off.cpu().numpy().view(np.uint64), host.offsets)
+        assert np.array_equal(m_ids.cpu().numpy().view(np.uint32), host.word_ids)
+        h = host_ms = b.host_ms()
+        assert h["download_ms"] >= 0 and host_ms["assemble_ms"] >= 0
+
+
+def _bench(args, env_extra=None, timeout=900):
+    import os
+    import subprocess
+    import sys
+
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, **(env_extra or {}))
+    return subprocess.run([sys.executable, str(root / "bench.py"), *args], capture_output=True, text=True,
+                          env=env, timeout=timeout, cwd=root)
+
+
+def test_bench_gpus_n_one_process():
+    """bench.py --gpus 2 without torchrun drives two shards from one process
+    (here both on device 0 via FPG_BENCH_DEVICES) and reports n_gpus = 2 and
+    the host gather cost inside e2e; without the override on a box with fewer
+    GPUs it fails loudly."""
+    import torch
+
+    r = _bench(["--config", "1", "--gpus", "2", "--steps", "2", "--warmup", "1", "--no-cpu-baseline"],
+               {"FPG_BENCH_DEVICES": "0,0"})
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "dict-shard x2"
+    assert len(line["shard_ms_per_step"]) == 2 and line["e2e"]["gather_ms_per_step"] is not None
+    if torch.cuda.device_count() < 3:
+        r = _bench(["--config", "1", "--gpus", "3", "--steps", "1", "--warmup", "1", "--no-cpu-baseline"])
+        assert r.returncode != 0 and "CUDA device" in (r.stderr + r.stdout)

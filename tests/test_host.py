@@ -32,7 +32,22 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), f"libfpg.so does not export {s}"
     assert set(syms) == set(FPG_SIGNATURES), "ctypes table out of sync with include/fpg.h"
-    assert lib.fpg_abi_version() == 2
+    assert lib.fpg_abi_version() == 3
+
+
+def test_python_capacity_equals_c_abi():
+    # Scheme.letter_capacity is host arithmetic (no libfpg.so load, so the
+    # reference arm of bench.py never maps the CUDA library); it must agree
+    # with fpg_letter_capacity on every parameterisation
+    from paper_1711_08475_b200.fingerprints import _letter_capacity
+
+    lib = load_fpg()
+    for v in range(5):
+        for w in (8, 16, 24, 32, 64, 128):
+            for b in range(-1, 9):
+                for p in range(-1, 70, 3):
+                    c = lib.fpg_letter_capacity(v, w, b, p)
+                    assert _letter_capacity(v, w, b, p) == (c if c >= 0 else -1), (v, w, b, p)
 
 
 def test_library_is_sm100a_cuda():

@@ -38,8 +38,19 @@ def _worker(rank, world, port, out_path):
     off, ids, _ = Oracle().query_batch(blob, offs, qb, qo, osch, 1, 1, True, True, threads=2)
     ids = ids + np.uint32(lo)  # rebase to global ids
     merged = gather_csr(off, ids)
+    # the point-to-point tensor gather of query_batch_distributed (NCCL on a
+    # GPU box; CPU tensors over gloo here), merged with the host merge
+    import torch
+
+    from paper_1711_08475_b200.sharding import gather_rows, merge_csr
+
+    parts = gather_rows(torch.from_numpy(off.view(np.int64)), torch.from_numpy(ids.view(np.int32)))
     if rank == 0:
+        m2 = merge_csr([(o.numpy().view(np.uint64), i.numpy().view(np.uint32)) for o, i in parts])
+        assert np.array_equal(m2[0], merged[0]) and np.array_equal(m2[1], merged[1])
         np.savez(out_path, off=merged[0], ids=merged[1])
+    else:
+        assert parts is None
     dist.barrier()
     dist.destroy_process_group()
 

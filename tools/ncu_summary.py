@@ -5,6 +5,7 @@ gpu__time_duration.sum --csv) and/or a --set full report of one kernel.
 usage: tools/ncu_summary.py launches <launches.csv>
        tools/ncu_summary.py report <prof.ncu-rep> [<src-lines>]
        tools/ncu_summary.py traffic <prof.ncu-rep> "<workload> <cell>" profiles/traffic.json
+       tools/ncu_summary.py sass <prof.ncu-rep>   (executed SASS by opcode and hottest blocks)
 """
 import collections
 import csv
@@ -109,9 +110,46 @@ def traffic(path, key, out_json):
     print(key, db[key])
 
 
+def sass(path, nblocks=12):
+    """Executed warp instructions by SASS opcode, and the hottest straight-line
+    blocks (runs of instructions with equal execution counts) with their mix."""
+    import re
+    src = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(src)))
+    hdr = next(r for r in rows if "Instructions Executed" in r)
+    data = rows[rows.index(hdr) + 1:]
+    ie, sc = hdr.index("Instructions Executed"), hdr.index("Source")
+
+    def op(txt):
+        t = re.sub(r"^@!?U?P\w+\s+", "", txt.strip())
+        return t.split()[0] if t else "?"
+    tot, byop, blocks, cur = 0, collections.Counter(), [], None
+    for i, r in enumerate(data):
+        if len(r) <= max(ie, sc):
+            continue
+        n = int(r[ie] or 0)
+        tot += n
+        byop[op(r[sc])] += n
+        if cur and cur[0] == n:
+            cur[2].append(op(r[sc]))
+        else:
+            cur = [n, i, [op(r[sc])]]
+            blocks.append(cur)
+    print(f"warp instructions executed: {tot}")
+    for o, n in byop.most_common(25):
+        print(f"  {o:22s} {n:14d} {100 * n / max(tot, 1):5.1f}%")
+    print("hottest blocks (start index, executions, length, share, mix):")
+    for n, i, ops in sorted(blocks, key=lambda b: -b[0] * len(b[2]))[:nblocks]:
+        mix = ", ".join(f"{k} {v}" for k, v in collections.Counter(ops).most_common(6))
+        print(f"  @{i:5d} x{n:10d} len {len(ops):4d} {100 * n * len(ops) / max(tot, 1):5.1f}%  {mix}")
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2])
+    elif sys.argv[1] == "sass":
+        sass(sys.argv[2])
     elif sys.argv[1] == "traffic":
         traffic(sys.argv[2], sys.argv[3], sys.argv[4])
     else:
