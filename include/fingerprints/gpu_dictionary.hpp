@@ -56,7 +56,7 @@ class GpuFingerprintedDictionary {
 public:
     GpuFingerprintedDictionary(std::vector<std::string> words, Scheme scheme, std::vector<int> devices = {0},
                                std::uint64_t id_base = 0)
-        : words_(std::move(words)), scheme_(std::move(scheme)), n_(words_.size()) {
+        : words_(std::move(words)), scheme_(std::move(scheme)), tables_(scheme_), n_(words_.size()) {
         std::vector<std::uint64_t> offs(words_.size() + 1, 0);
         std::string blob;
         for (std::size_t i = 0; i < words_.size(); ++i) {
@@ -90,6 +90,9 @@ public:
 
     [[nodiscard]] const std::vector<std::string>& words() const { return words_; }
     [[nodiscard]] const Scheme& scheme() const { return scheme_; }
+    /// dictionary.hpp:61: the host-side pair tables of the scheme (the GPU
+    /// scan applies the same F_D > 2k test bit-sliced).
+    [[nodiscard]] const ComparisonTables& tables() const { return tables_; }
     [[nodiscard]] std::size_t size() const { return n_; }
     [[nodiscard]] std::vector<Fingerprint> prints() const {
         std::vector<std::uint64_t> raw(n_);
@@ -146,12 +149,13 @@ public:
     }
 
 private:
-    explicit GpuFingerprintedDictionary(Scheme scheme) : scheme_(std::move(scheme)) {}
+    explicit GpuFingerprintedDictionary(Scheme scheme) : scheme_(std::move(scheme)), tables_(scheme_) {}
     struct Deleter {
         void operator()(fpg_dict* d) const { fpg_dict_destroy(d); }
     };
     std::vector<std::string> words_;
     Scheme scheme_;
+    ComparisonTables tables_;
     std::uint64_t n_ = 0;
     std::unique_ptr<fpg_dict, Deleter> dict_;
 };

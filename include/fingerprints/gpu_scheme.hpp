@@ -2,12 +2,25 @@
 //
 // Mirrors the reference's fingerprint.hpp interface: Variant / Metric (:14-15),
 // variant_supports (:36-38), Fingerprint (:41-44), Scheme (:57-162) and
-// render (:305-317), plus the fingerprint width W in {16, 32, 64} that the
-// reference fixes at 16 (:31).  build() runs on the GPU (K1 of libfpg.so);
-// the pairwise distance / can_reject of the reference live only inside the
-// GPU scan and are not offered on the host.
+// render (:305-317), ComparisonTables / fingerprint_distance /
+// lower_bound_errors / can_reject (:171-214, :287-301), plus the fingerprint
+// width W in {16, 32, 64} that the reference fixes at 16 (:31).  build()
+// runs on the GPU (K1 of libfpg.so); the pair test runs on the host here for
+// callers that test single pairs (the GPU scan evaluates the same F_D > 2k
+// rule bit-sliced, fpg_slice.cuh).
+//
+// This is the standalone API (no reference headers needed; Fingerprint::bits
+// is 64-bit so W = 32 / 64 fit).  Code that also includes the reference's own
+// headers uses fingerprints/b200_ref.hpp instead, which adds only the GPU
+// dictionary on top of the reference's types.
 #pragma once
+#ifdef FPG_B200_REF_HPP
+#error "fingerprints/b200.hpp (standalone) and fingerprints/b200_ref.hpp (reference extension) are exclusive"
+#endif
+#define FPG_B200_STANDALONE_HPP
 
+#include <array>
+#include <bit>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -142,6 +155,77 @@ private:
     unsigned b_, p_;
     int width_;
 };
+
+// ComparisonTables (fingerprint.hpp:171-214) generalised to W.  F_D of two
+// fingerprints: the popcount of their xor for occurrence / halved, the number
+// of fields with a non-zero xor for count / position (a +-1 counter step can
+// flip every bit of its field, so a field counts once).  At W = 16 the
+// reference's 2^16-entry tables are built; at W = 32 / 64 the same values
+// come from per-field masks (a table would not fit).
+class ComparisonTables {
+public:
+    explicit ComparisonTables(const Scheme& scheme) : width_(scheme.width()) {
+        for (unsigned d = 0; d < ceil_half_.size(); ++d) ceil_half_[d] = static_cast<std::uint8_t>((d + 1) / 2);
+        const Variant v = scheme.variant();
+        fields_ = v == Variant::Count || v == Variant::Position;
+        if (fields_)
+            for (std::size_t i = 0; i < scheme.field_count(); ++i) {
+                const unsigned w = scheme.field_width(i);
+                masks_.push_back((w >= 64 ? ~0ull : ((1ull << w) - 1)) << scheme.field_shift(i));
+            }
+        if (width_ == 16) {
+            popcount_.resize(1u << 16);
+            for (std::uint32_t x = 0; x < popcount_.size(); ++x)
+                popcount_[x] = static_cast<std::uint8_t>(std::popcount(x));
+            if (fields_) {
+                groups_.resize(1u << 16);
+                for (std::uint32_t x = 0; x < groups_.size(); ++x) groups_[x] = static_cast<std::uint8_t>(fold(x));
+            }
+        }
+    }
+
+    [[nodiscard]] int width() const { return width_; }
+    [[nodiscard]] int popcount16(std::uint16_t x) const {
+        return popcount_.empty() ? std::popcount(x) : popcount_[x];
+    }
+    [[nodiscard]] int ceil_half(int d) const { return ceil_half_[static_cast<std::size_t>(d)]; }
+    /// Mismatching-field count for an xor value (count / position schemes).
+    [[nodiscard]] int group_mismatch(std::uint64_t x) const {
+        return groups_.empty() ? fold(x) : groups_[static_cast<std::uint16_t>(x)];
+    }
+    [[nodiscard]] bool has_group_table() const { return fields_; }
+    /// Fingerprint distance of the scheme these tables were built for.
+    [[nodiscard]] int distance(Fingerprint a, Fingerprint b) const {
+        const std::uint64_t x = a.bits ^ b.bits;
+        if (fields_) return group_mismatch(x);
+        return width_ == 16 ? popcount_[static_cast<std::uint16_t>(x)] : std::popcount(x);
+    }
+
+private:
+    [[nodiscard]] int fold(std::uint64_t x) const {
+        int m = 0;
+        for (const std::uint64_t mask : masks_) m += (x & mask) != 0;
+        return m;
+    }
+    int width_;
+    bool fields_ = false;
+    std::vector<std::uint64_t> masks_;
+    std::vector<std::uint8_t> popcount_, groups_;
+    std::array<std::uint8_t, 65> ceil_half_{};
+};
+
+/// Fingerprint distance F_D (fingerprint.hpp:287-291).
+inline int fingerprint_distance(Fingerprint f1, Fingerprint f2, const Scheme&, const ComparisonTables& tables) {
+    return tables.distance(f1, f2);
+}
+
+/// Lower bound on the true number of errors: ceil(F_D / 2) (fingerprint.hpp:293-296).
+inline int lower_bound_errors(int fd, const ComparisonTables& tables) { return tables.ceil_half(fd); }
+
+/// True when the fingerprints alone prove the distance exceeds k (fingerprint.hpp:298-301).
+inline bool can_reject(Fingerprint f1, Fingerprint f2, int k, const Scheme& scheme, const ComparisonTables& tables) {
+    return lower_bound_errors(fingerprint_distance(f1, f2, scheme, tables), tables) > k;
+}
 
 inline SymbolFrequencyTable compute_frequencies_gpu(std::string_view text, int device) {
     SymbolFrequencyTable t;

@@ -53,3 +53,29 @@ def build_api_check(tmp_dir: Path) -> Path:
                     str(ROOT / "tests" / "cpp" / "api_check.cpp"), f"-L{LIBFPG.parent}", "-lfpg",
                     f"-Wl,-rpath,{LIBFPG.parent}", "-o", str(exe)], check=True)
     return exe
+
+
+REF_INCLUDE = Path("/root/reference/proj/include")
+API_CHECK_REF_BIN = ROOT / "tests" / "cpp" / "_bin" / "api_check_ref"
+
+
+def build_api_check_ref(out: Path = API_CHECK_REF_BIN) -> Path:
+    """Compiles tests/cpp/api_check_ref.cpp: the reference's own headers
+    (corpus / dictionary / reference.hpp, from /root/reference) and
+    include/fingerprints/b200_ref.hpp in one translation unit, linked with
+    libfpg.so.  Needs the reference tree (this container); __graft_entry__.build()
+    leaves the binary in tests/cpp/_bin/ so it travels to the GPU box."""
+    import shutil
+    import subprocess
+
+    from paper_1711_08475_b200._lib import LIBFPG
+
+    cxx = shutil.which("g++")
+    if not cxx or not (REF_INCLUDE / "fingerprints" / "dictionary.hpp").exists():
+        raise FileNotFoundError("g++ or the reference headers are missing")
+    out.parent.mkdir(parents=True, exist_ok=True)
+    subprocess.run([cxx, "-std=c++20", "-O2", "-Wall", "-Werror", f"-I{REF_INCLUDE}", f"-I{ROOT / 'include'}",
+                    str(ROOT / "tests" / "cpp" / "api_check_ref.cpp"), f"-L{LIBFPG.parent}", "-lfpg",
+                    "-Wl,-rpath,$ORIGIN/../../../paper_1711_08475_b200/lib", f"-Wl,-rpath,{LIBFPG.parent}",
+                    "-o", str(out)], check=True)
+    return out

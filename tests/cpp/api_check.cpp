@@ -56,6 +56,34 @@ static int host_checks() {
     const auto freq = compute_frequencies(std::vector<std::string>{"banana", "bandana", "cab"});
     const LetterSet common = select_letters(freq, 2, LetterStrategy::Common);
     CHECK(common.symbols() == "an");
+    // ComparisonTables / fingerprint_distance / can_reject generalised to W
+    // (fingerprint.hpp:171-214, :287-301) vs a field-by-field count
+    // (reference.hpp:62-84 restated with 16 -> W)
+    std::mt19937_64 rng(3);
+    const std::string az = "abcdefghijklmnopqrstuvwxyz0123456789ABCDEFGHIJKLMNOPQRSTUVWXYZ!?";
+    for (int width : {16, 32, 64})
+        for (Variant v : {Variant::Occurrence, Variant::OccurrenceHalved, Variant::Count, Variant::Position}) {
+            const unsigned b = v == Variant::Count && width == 64 ? 4 : 2;
+            const std::size_t cap = Scheme::letter_capacity(v, b, 3, width);
+            const Scheme s = Scheme::make(v, LetterSet(az.substr(0, cap)), b, 3, width);
+            const ComparisonTables t(s);
+            CHECK(t.width() == width && t.has_group_table() == (v == Variant::Count || v == Variant::Position));
+            const std::uint64_t wmask = width == 64 ? ~0ull : (1ull << width) - 1;
+            for (int i = 0; i < 4000; ++i) {
+                const Fingerprint x{rng() & wmask}, y{(rng() & rng()) & wmask};
+                const std::uint64_t d = x.bits ^ y.bits;
+                int fd = 0;
+                if (t.has_group_table()) {
+                    for (std::size_t f = 0; f < s.field_count(); ++f)
+                        fd += ((d >> s.field_shift(f)) & ((1ull << s.field_width(f)) - 1)) != 0;
+                } else {
+                    for (int bit = 0; bit < width; ++bit) fd += (d >> bit) & 1;
+                }
+                CHECK(fingerprint_distance(x, y, s, t) == fd);
+                CHECK(lower_bound_errors(fd, t) == (fd + 1) / 2);
+                for (int k = 0; k <= 3; ++k) CHECK(can_reject(x, y, k, s, t) == ((fd + 1) / 2 > k));
+            }
+        }
     std::puts("api_check host: ok");
     return 0;
 }
@@ -114,6 +142,10 @@ static int gpu_checks() {
             CHECK(st.compared == words.size() && st.matches == want.size());
             CHECK(st.rejected_by_length + st.rejected_by_fingerprint + st.verified == st.compared);
             CHECK(per[q].verified == st.verified && per[q].rejected_by_length == st.rejected_by_length);
+            // every match survives the host pair test with the dictionary's tables()
+            const Fingerprint qp = build(queries[q], scheme);
+            const std::vector<Fingerprint> prints = dict.prints();
+            for (std::size_t id : got) CHECK(!can_reject(qp, prints[id], 1, scheme, dict.tables()));
         }
     }
     // the same dictionary split from its newline text on the GPU

@@ -330,6 +330,28 @@ def test_cpp_drop_in_queries(tmp_path):
     assert "api_check gpu: ok" in out.stdout
 
 
+@pytest.mark.gpu
+def test_cpp_reference_extension():
+    """Reference caller code with the reference's FingerprintedDictionary,
+    naive_scan and the GPU dictionary (b200_ref.hpp) in one translation
+    unit: prints, matches and QueryStats equal for every variant x metric
+    the reference filters, and every GPU match passes the reference's
+    can_reject with the GPU dictionary's tables() (tests/cpp/api_check_ref.cpp,
+    prebuilt by __graft_entry__.build() where the reference tree exists)."""
+    import subprocess
+
+    from conftest import API_CHECK_REF_BIN, REF_INCLUDE, build_api_check_ref
+
+    exe = API_CHECK_REF_BIN
+    if (REF_INCLUDE / "fingerprints" / "dictionary.hpp").exists():
+        exe = build_api_check_ref()
+    if not exe.exists():
+        pytest.skip("api_check_ref was not prebuilt (no reference tree where build() ran)")
+    out = subprocess.run([str(exe), "gpu"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr + out.stdout
+    assert "api_check_ref gpu: ok" in out.stdout
+
+
 @pytest.mark.parametrize("text", [b"", b"\n", b"a", b"a\n", b"a\n\nbc\r\nd", b"\n\n\n", b"xy\nz"])
 def test_dictionary_from_text_edges(text):
     """fpg_dict_create_from_text splits like read_word_lines (corpus.hpp:116-125)."""

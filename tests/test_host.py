@@ -185,6 +185,23 @@ def test_subsample():
     assert idx.tolist() == [0, 2, 4] and bytes(b) == b"accce"
 
 
+def test_cpp_reference_extension_host(tmp_path):
+    """include/fingerprints/b200_ref.hpp compiles in ONE translation unit with
+    the reference's corpus.hpp, dictionary.hpp and reference.hpp (no type
+    collision), and the reference-side pair test it exposes agrees with
+    reference.hpp's field-by-field distance."""
+    import subprocess
+
+    from conftest import REF_INCLUDE, build_api_check_ref
+
+    if not (REF_INCLUDE / "fingerprints" / "dictionary.hpp").exists():
+        pytest.skip("reference headers absent")
+    exe = build_api_check_ref(tmp_path / "api_check_ref")
+    out = subprocess.run([str(exe), "host"], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr + out.stdout
+    assert "api_check_ref host: ok" in out.stdout
+
+
 def test_product_never_imports_the_oracle():
     """Only tests/, smoke() and bench.py's CPU legs may touch oracle/."""
     for path in (ROOT / "paper_1711_08475_b200").rglob("*.py"):
