@@ -640,9 +640,9 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         // resident CTA.
         const uint32_t grp = (uint32_t)fpg::slice_group_slabs(D->npt);
         uint32_t per = 32 * grp, qchunk = fpg::kSliceQ;
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, sh.device);
         {
-            int sms = 148;
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, sh.device);
             const uint64_t target = (uint64_t)sms * 2 * 4;
             auto count_tiles = [&]() {
                 uint64_t c = 0;
@@ -700,8 +700,12 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
                 add(lw, qe, (uint32_t)nq, true);
             }
         }
-        // Largest tiles first; the last ~30% of the work is cut into quarter
-        // tiles so the dynamically scheduled grid drains evenly.
+        // Largest tiles first; the tail of the schedule is cut into 32- and
+        // 16-query tiles so the dynamically scheduled grid drains evenly.  A
+        // small plan cuts everything after FPG_TAIL_A / FPG_TAIL_B of its
+        // work; a large one only about its last 4 tiles per resident CTA
+        // (small tiles cost a slab-group load per few queries: config 5 has
+        // ~6e5 tiles and needs no cutting before its very end).
         auto cost = [](const fpg::SliceTile& x) { return (uint64_t)x.q_count * x.n_slabs; };
         std::stable_sort(splan.begin(), splan.end(),
                          [&](const fpg::SliceTile& x, const fpg::SliceTile& y) { return cost(x) > cost(y); });
@@ -709,7 +713,9 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         for (const auto& t : splan) work += cost(t);
         std::vector<fpg::SliceTile> fine;
         fine.reserve(splan.size() + splan.size() / 2);
-        static const double tail_a = env_double("FPG_TAIL_A", 0.35), tail_b = env_double("FPG_TAIL_B", 0.85);
+        static const double env_a = env_double("FPG_TAIL_A", 0.35), env_b = env_double("FPG_TAIL_B", 0.85);
+        const double tail_f = std::min(1.0, 4.0 * 2 * sms / std::max<double>(1.0, (double)splan.size()));
+        const double tail_a = 1.0 - (1.0 - env_a) * tail_f, tail_b = 1.0 - (1.0 - env_b) * tail_f;
         for (const auto& t : splan) {
             acc += cost(t);
             const uint32_t sub = acc <= tail_a * work ? t.q_count : acc <= tail_b * work ? 32u : 16u;
@@ -1137,7 +1143,7 @@ void download(fpg_batch* B, fpg_result* out) {
 
 // Chooses the K2 path and the sig' map: non-letter bytes of the dictionary,
 // ranked by frequency (descending, then byte), dealt round robin onto S
-// one-bit fields (S = 0 / 8 / 12 / 16 by how many such bytes exist; FPG_SIGP_BITS
+// one-bit fields (S = 0 / 8 / 10 / 12 / 16 by how many such bytes exist; FPG_SIGP_BITS
 // overrides).  FPG_SLICE=0 selects the generic k_scan for A/B runs.
 void configure_slice(fpg_dict& D, const std::vector<unsigned long long>& hist) {
     const char* e = std::getenv("FPG_SLICE");
@@ -1146,7 +1152,7 @@ void configure_slice(fpg_dict& D, const std::vector<unsigned long long>& hist) {
     for (int c = 0; c < 256; ++c)
         if (hist[c] && D.params.slot[c] < 0) others.push_back(c);
     std::stable_sort(others.begin(), others.end(), [&](int a, int b) { return hist[a] > hist[b]; });
-    auto snap = [](size_t v) { return v == 0 ? 0 : v <= 8 ? 8 : v <= 12 ? 12 : 16; };
+    auto snap = [](size_t v) { return v == 0 ? 0 : v <= 8 ? 8 : v <= 10 ? 10 : v <= 12 ? 12 : 16; };
     // W = 32 takes at most 12 sig' fields: NPT = 44 leaves one slab per lane,
     // yet every W = 32 cell of configs 3 and 5 ran 4-10% faster than with 8
     // (fewer candidates).  No sig' when it cannot pay (measured): <= 4 other

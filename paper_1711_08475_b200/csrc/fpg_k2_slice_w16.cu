@@ -10,18 +10,20 @@ namespace {
 template <int NP, int FW, int EXTRA, int S>
 void launch_slice(const fpg::SliceTile* tiles, uint32_t ntiles, const fpg::SliceParams& P, cudaStream_t st,
                   int device) {
-    auto kern = fpg::k_slice<NP, FW, EXTRA, S>;
+    // the common options (filter + stats + window on, k = 1) run the HOT instantiation
+    const bool hot = P.use_fp && P.stats && P.wskip && !P.exhaustive && P.k == 1;
+    auto kern = hot ? fpg::k_slice<NP, FW, EXTRA, S, true> : fpg::k_slice<NP, FW, EXTRA, S, false>;
     constexpr size_t smem = fpg::slice_smem_bytes(NP + S);
-    static int resident[64] = {0};  // per device: CTAs resident on the whole GPU (0 = not yet queried)
+    static int resident[2][64] = {{0}};  // per variant and device: CTAs resident on the whole GPU (0 = not queried)
     const int dv = device & 63;
-    if (!resident[dv]) {
+    if (!resident[hot][dv]) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int sms = 148, per_sm = 0;
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, fpg::kSliceThreads, smem));
-        resident[dv] = sms * std::max(per_sm, 1);
+        resident[hot][dv] = sms * std::max(per_sm, 1);
     }
-    const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)resident[dv]);
+    const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)resident[hot][dv]);
     kern<<<(unsigned)std::max<uint64_t>(grid, 1), fpg::kSliceThreads, smem, st>>>(tiles, ntiles, P);
     CK(cudaGetLastError());
 }
@@ -32,6 +34,7 @@ void launch_slice_s(int nsig, const fpg::SliceTile* tiles, uint32_t ntiles, cons
     switch (nsig) {
         case 0: launch_slice<NP, FW, EXTRA, 0>(tiles, ntiles, P, st, device); break;
         case 8: launch_slice<NP, FW, EXTRA, 8>(tiles, ntiles, P, st, device); break;
+        case 10: launch_slice<NP, FW, EXTRA, 10>(tiles, ntiles, P, st, device); break;
         case 12: launch_slice<NP, FW, EXTRA, 12>(tiles, ntiles, P, st, device); break;
         default: launch_slice<NP, FW, EXTRA, 16>(tiles, ntiles, P, st, device); break;
     }

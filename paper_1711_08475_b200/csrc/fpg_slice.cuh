@@ -167,11 +167,20 @@ __host__ __device__ constexpr size_t slice_smem_bytes(int npt) {
            4u * kSliceWarpBuf * kSliceWarps + 2u * kSliceQ * kSliceWarps;
 }
 
-template <int NP, int FW, int EXTRA, int S>
+// HOT: the options of the common run fixed at compile time (fingerprint
+// filter on, QueryStats on, weight window on, k = 1, not exhaustive), so the
+// per-step code carries no uniform branches on them; other runs take the
+// generic instantiation (HOT = false), which reads them from P.
+template <int NP, int FW, int EXTRA, int S, bool HOT>
 __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __restrict__ tiles, uint32_t ntiles,
                                                             const __grid_constant__ SliceParams P) {
     using Sh = SliceShape<NP, FW, EXTRA, S>;
     constexpr int NPT = Sh::NPT, SL = Sh::SL, NF = Sh::NF;
+    const bool o_use_fp = HOT || P.use_fp;
+    const bool o_stats = HOT || P.stats;
+    const bool o_wskip = HOT || P.wskip;
+    const bool o_exhaustive = !HOT && P.exhaustive;
+    const int o_k = HOT ? 1 : P.k;
     extern __shared__ __align__(16) uint8_t smem[];
     uint2* s_qm = reinterpret_cast<uint2*>(smem);                           // [kSliceQ][NPT] (s, m)
     uint4* s_qb = reinterpret_cast<uint4*>(s_qm + kSliceQ * NPT);           // [kSliceQ][2]: bytes 0..31
@@ -219,12 +228,13 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
             s_qinfo[j] = (uint32_t)m;
             s_qid[j] = id;
             s_surv[j] = 0u;
-            s_qw[j] = P.wskip ? P.q_weight[qp] : 0u;
+            s_qw[j] = o_wskip ? P.q_weight[qp] : 0u;
         }
         // this lane's slabs of slab group g (SL rows of 32 slabs), the
         // group's valid words and its group-weight box
         uint32_t pl[SL][NPT];
         uint32_t valid[SL];
+        const uint32_t* planes = P.planes + tl.plane_base;  // the tile's bucket
         uint32_t vw = 0;
         uint2 box = make_uint2(0u, 0u);
         const uint32_t n_grp = (tl.n_slabs + 32u * SL - 1u) / (32u * SL);
@@ -236,13 +246,19 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 const uint32_t rel = 32u * (SL * g + r) + (uint32_t)lane;
                 const uint32_t slab = tl.slab_begin + rel;
                 const bool ok = rel < tl.n_slabs;
-                const uint32_t* src = P.planes + tl.plane_base + slab;
+                // lanes past the tile's end load the tile's first slab (valid
+                // memory; valid[r] = 0 masks every result of theirs): one
+                // pointer step per plane, no per-plane predication
+                const uint32_t* src = planes + (ok ? slab : tl.slab_begin);
 #pragma unroll
-                for (int b = 0; b < NPT; ++b) pl[r][b] = ok ? __ldg(src + (size_t)b * tl.ns) : 0u;
+                for (int b = 0; b < NPT; ++b) {
+                    pl[r][b] = __ldg(src);
+                    src += tl.ns;
+                }
                 const uint32_t rem = tl.w_count - 32u * slab;  // words left in the bucket from this slab on
                 valid[r] = !ok ? 0u : rem >= 32u ? 0xffffffffu : ((1u << rem) - 1u);
                 vw += __popc(valid[r]);
-                if (ok && P.wskip) {
+                if (ok && o_wskip) {
                     const uint2 mm = __ldg(P.slab_w + tl.slab_g0 + slab);
                     wlo = __vminu4(wlo, mm.x);
                     whi = __vmaxu4(whi, mm.y);
@@ -334,19 +350,19 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                                 const uint4 qa = s_qb[2 * j];
                                 a4[0] = qa.x; a4[1] = qa.y; a4[2] = qa.z; a4[3] = qa.w;
                                 b4[0] = bw[u][0]; b4[1] = bw[u][1]; b4[2] = bw[u][2]; b4[3] = bw[u][3];
-                                hit = verify_regs<4>(a4, b4, m, n, P.k);
+                                hit = verify_regs<4>(a4, b4, m, n, o_k);
                             } else if (mx <= 32) {
                                 uint32_t a8[8];
                                 const uint4 qa = s_qb[2 * j], qc = s_qb[2 * j + 1];
                                 a8[0] = qa.x; a8[1] = qa.y; a8[2] = qa.z; a8[3] = qa.w;
                                 a8[4] = qc.x; a8[5] = qc.y; a8[6] = qc.z; a8[7] = qc.w;
-                                hit = verify_regs<8>(a8, bw[u], m, n, P.k);
+                                hit = verify_regs<8>(a8, bw[u], m, n, o_k);
                             } else {
                                 const uint32_t qpos = tl.q_begin + j;
                                 const int qs = stride_of_len(m);
                                 const uint8_t* qb = P.q_bytes + P.q_bbase[m] + (uint64_t)(qpos - P.q_start[m]) * qs;
                                 const uint8_t* wb = P.w_bytes + tl.w_bytes + (uint64_t)widx * tl.w_stride;
-                                hit = verify_pair(qb, m, qs, wb, n, tl.w_stride, P.k);
+                                hit = verify_pair(qb, m, qs, wb, n, tl.w_stride, o_k);
                             }
                         }
                         const uint32_t hb = __ballot_sync(0xffffffffu, hit);
@@ -461,13 +477,13 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                         for (int r = 0; r < SLX; ++r) add2(h, r, fbit(h, r, i), i + 1 < I1 ? fbit(h, r, i + 1) : 0u);
             };
             auto rejected = [&](int h, int r) -> uint32_t {
-                return P.k ? cf[h][r] | (ct[h][r] & co[h][r]) : cf[h][r] | ct[h][r] | co[h][r];
+                return o_k ? cf[h][r] | (ct[h][r] & co[h][r]) : cf[h][r] | ct[h][r] | co[h][r];
             };
             // scheme fields.  Skipped when they do not bound the metric (halved
             // / position with Levenshtein, filter off): sig' alone stays a
             // valid bound.
-            if (P.use_fp) count(std::integral_constant<int, 0>{}, std::integral_constant<int, NF + EXTRA>{});
-            if (P.stats) {  // fingerprint survivors: QueryStats::verified (dictionary.hpp:102-110)
+            if (o_use_fp) count(std::integral_constant<int, 0>{}, std::integral_constant<int, NF + EXTRA>{});
+            if (o_stats) {  // fingerprint survivors: QueryStats::verified (dictionary.hpp:102-110)
                 uint32_t sv = 0;  // query h in bits [16 h, 16 h + 16): <= 2048 per warp
 #pragma unroll
                 for (int h = 0; h < NQ; ++h)
@@ -484,13 +500,13 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 }
             }
             if (verify) {
-                if (!P.exhaustive)
+                if (!o_exhaustive)
                     count(std::integral_constant<int, NF + EXTRA>{}, std::integral_constant<int, NF + EXTRA + S>{});
 #pragma unroll
                 for (int h = 0; h < NQ; ++h)
 #pragma unroll
                     for (int r = 0; r < SLX; ++r) {
-                        const uint32_t cand = P.exhaustive ? valid[r] : valid[r] & ~rejected(h, r);
+                        const uint32_t cand = o_exhaustive ? valid[r] : valid[r] & ~rejected(h, r);
                         if (cand) {
                             s_queue[qn * kSliceThreads + tid] = make_uint2(jq[h] | ((row0 + (uint32_t)r) << 16), cand);
                             ++qn;
@@ -511,7 +527,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
         // have F_D > 2k with every word of the group: sum_g |group weight
         // difference| <= F_D).
         {
-            const uint32_t span = 2u * (uint32_t)P.k;
+            const uint32_t span = 2u * (uint32_t)o_k;
             uint16_t* ql = s_qlist + warp * kSliceQ;
             for (bool first = true;; first = false) {
                 if (!first) {
@@ -526,7 +542,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 for (uint32_t b = 0; b < tl.q_count; b += 32) {
                     const uint32_t j = b + (uint32_t)lane;
                     bool in = j < tl.q_count;
-                    if (in && P.wskip) in = box_dist(s_qw[j], box) <= span;
+                    if (in && o_wskip) in = box_dist(s_qw[j], box) <= span;
                     const uint32_t bal = __ballot_sync(0xffffffffu, in);
                     if (in) ql[nlist + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)j;
                     nlist += __popc(bal);
@@ -549,12 +565,12 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
         }
         if (verify) flush();
         __syncthreads();  // tile consumed; s_next[it & 1] and s_surv complete
-        if (P.stats)
+        if (o_stats)
             for (uint32_t j = tid; j < tl.q_count; j += kSliceThreads)
                 if (s_surv[j]) atomicAdd(&P.q_survivors[s_qid[j]], s_surv[j]);
         t = s_next[it & 1];
     }
-    if (P.stats && lane == 0 && surv_warp) atomicAdd(P.survivors_total, surv_warp);
+    if (o_stats && lane == 0 && surv_warp) atomicAdd(P.survivors_total, surv_warp);
     oc.close(P.out, P.out_cap);
     if (lane == 0 && oc.real) atomicAdd(P.match_total, (unsigned long long)oc.real);
     if (lane == 0 && scanned_warp) atomicAdd(P.scanned, scanned_warp);

@@ -395,9 +395,8 @@ def test_full_size_configs_vs_oracle(oracle, cfg, cell, nsample):
     evenly spaced query subsample is checked against the oracle (ids and
     QueryStats), plus the batch total against the filter-off run."""
     import bench
-    from paper_1711_08475_b200.corpus import CELLS
-
-    c, blob, offs, qblob, qoffs, scheme, metric, first, n = bench.workload(cfg, cell, 0, 1)
+    w = bench.Workload(cfg, cell)  # the bench's workload: letters and query sources over the whole dictionary
+    blob, offs, qblob, qoffs, scheme, metric = w.blob, w.offs, w.qblob, w.qoffs, w.scheme, w.metric
     nq = len(qoffs) - 1
     opt = QueryOptions(metric, 1, True, True)
     with GpuFingerprintedDictionary((blob, offs), scheme, keep_words=False) as d:
