@@ -632,14 +632,17 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         // Tiles = (<= kSliceMaxSlabs slabs) x (<= kSliceQ queries), largest first,
         // handed out by an atomic counter.
         const int L1 = fpg::kMaxLen + 1;
-        // Tile shape: 128 queries x 32 slab groups (the warps claim the tile's
+        // Tile shape: 128 queries x 128 slab groups (the warps claim the tile's
         // groups dynamically, so one tile's query masks serve many groups),
         // made smaller (slabs down to two groups per warp, queries down to 32,
         // slabs down to one group per warp, queries down to 16, then slabs down
         // to one group) while the batch would give fewer than ~4 tiles per
         // resident CTA.
         const uint32_t grp = (uint32_t)fpg::slice_group_slabs(D->npt);
-        uint32_t per = 32 * grp, qchunk = fpg::kSliceQ;
+        // FPG_TILE_GROUPS: slab groups per full tile (A/B runs); 128 = 16 per
+        // warp, so the end-of-tile barrier waits on a smaller share of the tile
+        static const uint32_t tile_groups = (uint32_t)env_double("FPG_TILE_GROUPS", 128.0);
+        uint32_t per = tile_groups * grp, qchunk = fpg::kSliceQ;
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, sh.device);
         {

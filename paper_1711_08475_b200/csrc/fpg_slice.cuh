@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
     __shared__ uint32_t s_surv[kSliceQ];
     __shared__ uint32_t s_qw[kSliceQ];  // query group weights
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    unsigned long long surv_warp = 0;  // lane 0: the warp's fingerprint survivors
+    unsigned long long surv_warp = 0;  // lanes 0, 1: the warp's fingerprint survivors
     uint32_t cand_lane = 0;
     unsigned long long scanned_warp = 0;  // lane 0
     OutChunk oc;
@@ -490,13 +490,11 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
 #pragma unroll
                     for (int r = 0; r < SLX; ++r) sv += (uint32_t)__popc(valid[r] & ~rejected(h, r)) << (16 * h);
                 sv = __reduce_add_sync(0xffffffffu, sv);
-                if (lane == 0) {
-#pragma unroll
-                    for (int h = 0; h < NQ; ++h) {
-                        const uint32_t v = (sv >> (16 * h)) & 0xffffu;
-                        if (v) atomicAdd(&s_surv[jq[h]], v);
-                        surv_warp += v;
-                    }
+                static_assert(NQ <= 2, "two queries per step at most");
+                if (lane < NQ) {  // lane h posts query h's count: one atomic instruction per step
+                    const uint32_t v = (sv >> (16 * lane)) & 0xffffu;
+                    if (v) atomicAdd(&s_surv[lane ? jq[NQ - 1] : jq[0]], v);
+                    surv_warp += v;
                 }
             }
             if (verify) {
@@ -570,7 +568,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 if (s_surv[j]) atomicAdd(&P.q_survivors[s_qid[j]], s_surv[j]);
         t = s_next[it & 1];
     }
-    if (o_stats && lane == 0 && surv_warp) atomicAdd(P.survivors_total, surv_warp);
+    if (o_stats && lane < 2 && surv_warp) atomicAdd(P.survivors_total, surv_warp);
     oc.close(P.out, P.out_cap);
     if (lane == 0 && oc.real) atomicAdd(P.match_total, (unsigned long long)oc.real);
     if (lane == 0 && scanned_warp) atomicAdd(P.scanned, scanned_warp);
