@@ -804,6 +804,8 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         SP.q_weight = Q.wt.p;
         SP.slab_w = W.slab_w.p;
         SP.scanned = S.counters.p + 6;
+        static const int drop = (int)env_double("FPG_DROP_CANDIDATES", 0.0);
+        SP.drop_candidates = drop;
     } else {
         // comparison words: the reference-layout fingerprints when the
         // collections were built for k_slice (no one-hot form, no signatures)

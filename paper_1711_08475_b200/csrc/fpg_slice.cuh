@@ -129,6 +129,7 @@ struct SliceParams {
     const uint2* slab_w;        // per global slab: per-byte min / max of its words' group weights
     unsigned long long* scanned;  // pairs actually evaluated (after the weight skip)
     int32_t exhaustive;         // verify every pair: no fingerprint / sig' pruning (naive-path timing)
+    int32_t drop_candidates;    // A/B diagnosis only (FPG_DROP_CANDIDATES=1): queued candidates are discarded unverified
 };
 
 __device__ __forceinline__ int stride_of_len(int len) { return len <= 16 ? 16 : (len + 15) & ~15; }
@@ -137,6 +138,13 @@ __device__ __forceinline__ int stride_of_len(int len) { return len <= 16 ? 16 : 
 __device__ __forceinline__ uint32_t qxor(uint32_t p, uint32_t s, uint32_t m) { return p * s + m; }
 // bitwise majority (the carry of a full adder): one LOP3
 __device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (c & (a | b)); }
+// One LOP3 with an explicit truth table (a = 0xf0, b = 0xcc, c = 0xaa).
+template <uint32_t LUT>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+    return d;
+}
 // Per-byte min of lo and max of hi over the warp: a group-weight box.
 __device__ __forceinline__ uint2 warp_box(uint32_t lo, uint32_t hi) {
 #pragma unroll
@@ -283,6 +291,10 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
         uint32_t* wbuf = s_wbuf + warp * kSliceWarpBuf;
         auto flush = [&]() {
             __syncwarp();
+            if (P.drop_candidates) {
+                qn = 0;
+                return;
+            }
             for (;;) {
                 // pending candidate bits of this lane
                 uint32_t c = 0;
@@ -404,12 +416,18 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
             // o = ones bit, t = twos bit, f = "F >= 4".  Field bits enter four
             // at a time (two full adders into o, one into t: 7 LOP3 per 4
             // fields) or two at a time (4 LOP3); reject at k = 1 is
-            // F >= 3 = f | (t & o), at k = 0 F >= 1 = f | t | o.
+            // F >= 3 = f | (t & o), at k = 0 F >= 1 = f | t | o.  f starts as
+            // the complement of the valid words (a slab's words past the
+            // bucket's end are rejected), so a pass / candidate mask is one
+            // LOP3: ~(f | (t & o)).
             uint32_t co[NQ][SLX], ct[NQ][SLX], cf[NQ][SLX];
 #pragma unroll
             for (int h = 0; h < NQ; ++h)
 #pragma unroll
-                for (int r = 0; r < SLX; ++r) co[h][r] = ct[h][r] = cf[h][r] = 0u;
+                for (int r = 0; r < SLX; ++r) {
+                    co[h][r] = ct[h][r] = 0u;
+                    cf[h][r] = ~valid[r];  // folded into the first LOP3 that reads it
+                }
             // (s, m) of plane b for query h
 #define FPG_QS(h, b) ((b) & 1 ? qm[h][(b) >> 1].z : qm[h][(b) >> 1].x)
 #define FPG_QM(h, b) ((b) & 1 ? qm[h][(b) >> 1].w : qm[h][(b) >> 1].y)
@@ -476,8 +494,9 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
 #pragma unroll
                         for (int r = 0; r < SLX; ++r) add2(h, r, fbit(h, r, i), i + 1 < I1 ? fbit(h, r, i + 1) : 0u);
             };
-            auto rejected = [&](int h, int r) -> uint32_t {
-                return o_k ? cf[h][r] | (ct[h][r] & co[h][r]) : cf[h][r] | ct[h][r] | co[h][r];
+            // words that pass: ~(f | (t & o)) at k = 1, ~(f | t | o) at k = 0 (one LOP3)
+            auto passed = [&](int h, int r) -> uint32_t {
+                return o_k ? lop3<0x07>(cf[h][r], ct[h][r], co[h][r]) : lop3<0x01>(cf[h][r], ct[h][r], co[h][r]);
             };
             // scheme fields.  Skipped when they do not bound the metric (halved
             // / position with Levenshtein, filter off): sig' alone stays a
@@ -488,10 +507,10 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
 #pragma unroll
                 for (int h = 0; h < NQ; ++h)
 #pragma unroll
-                    for (int r = 0; r < SLX; ++r) sv += (uint32_t)__popc(valid[r] & ~rejected(h, r)) << (16 * h);
+                    for (int r = 0; r < SLX; ++r) sv += (uint32_t)__popc(passed(h, r)) << (16 * h);
                 sv = __reduce_add_sync(0xffffffffu, sv);
                 static_assert(NQ <= 2, "two queries per step at most");
-                if (lane < NQ) {  // lane h posts query h's count: one atomic instruction per step
+                if (lane < NQ) {
                     const uint32_t v = (sv >> (16 * lane)) & 0xffffu;
                     if (v) atomicAdd(&s_surv[lane ? jq[NQ - 1] : jq[0]], v);
                     surv_warp += v;
@@ -504,7 +523,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 for (int h = 0; h < NQ; ++h)
 #pragma unroll
                     for (int r = 0; r < SLX; ++r) {
-                        const uint32_t cand = o_exhaustive ? valid[r] : valid[r] & ~rejected(h, r);
+                        const uint32_t cand = o_exhaustive ? valid[r] : passed(h, r);
                         if (cand) {
                             s_queue[qn * kSliceThreads + tid] = make_uint2(jq[h] | ((row0 + (uint32_t)r) << 16), cand);
                             ++qn;
