@@ -333,7 +333,7 @@ __device__ __forceinline__ void count_match(uint32_t* q_matches, uint32_t qid, u
 // Per-warp output chunk: a warp reserves kOutChunk key slots with one atomic
 // and fills them over many ballots; slots it leaves unused hold kNoKey (K4
 // skips them).  Keeps the global slot counter out of the per-hit path.
-constexpr uint32_t kOutChunk = 64;
+constexpr uint32_t kOutChunk = 256;
 constexpr unsigned long long kNoKey = ~0ull;
 
 struct OutChunk {
