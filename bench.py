@@ -93,6 +93,29 @@ def ops_per_comparison(scheme, sig_fields: int) -> float:
     return (ors + csa(nf + extra) + csa(sig_fields) + 1) / 32.0
 
 
+def hbm_peak():
+    """(GB/s, basis): the driver-measured copy bandwidth of this pool's B200s
+    (MEASURED_PEAKS.json), else the B200_PROFILING.md fallback."""
+    try:
+        rec = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(rec["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (driver: torch copy, read + write bytes)"
+    except (OSError, ValueError, KeyError):
+        return 7700.0, "fallback: nominal B200 HBM3e (MEASURED_PEAKS.json absent)"
+
+
+def construction_roofline(d) -> dict:
+    """HBM roofline of dictionary construction (shard 0): per stage, the
+    CUDA-event time and algorithmic bytes from fpg_dict_build_profile."""
+    peak, basis = hbm_peak()
+    stages = []
+    for st in d.build_profile(0):
+        gbs = st["bytes"] / (st["ms"] * 1e6) if st["ms"] > 0 else None
+        stages.append({"stage": st["name"], "ms": st["ms"], "algorithmic_bytes": st["bytes"], "gbs": gbs,
+                       "frac": gbs / peak if gbs else None})
+    return {"bound": "hbm", "peak_gbs": peak, "peak_basis": basis, "stages": stages,
+            "note": "cub_radix_sort is CUB's onesweep (library); bytes = one key+value read+write per 8-bit pass"}
+
+
 def profiled_traffic(workload: str, cell: str):
     """DRAM bytes of one K2 launch from the committed ncu --set full capture
     (profiles/traffic.json, written by tools/ncu_summary.py traffic)."""
@@ -506,6 +529,7 @@ def main():
         "matches_per_step": int(csr.offsets[-1]) if world == 1 else None,
         "shard_ms_per_step": [statistics.mean(s[i] for s in shard_ms) for i in range(nsh)],
         "construction_s": build_s, "setup_s": w.setup_s,
+        "construction": construction_roofline(d),
         "gpu_launches": launches,
         "e2e": e2e,
         "roofline": {"bound": bound, "kernel": "k_slice (K2 filter+verify)" if shape["sliced"] else "k_scan (K2)",

@@ -126,6 +126,18 @@ int fpg_dict_size(const fpg_dict* dict, uint64_t* n);
 int fpg_dict_prints(const fpg_dict* dict, uint64_t* out);
 /* Seconds the construction took (upload + K1 + layout), like bench.hpp:118-120. */
 int fpg_dict_build_seconds(const fpg_dict* dict, double* seconds);
+/* Construction stages of one shard (k_lengths, k_weight_keys, cub_radix_sort,
+ * k_build, k_planes): device time from CUDA events on the build stream and
+ * the stage's algorithmic HBM bytes (reads + writes).  Writes min(cap, n)
+ * entries and sets *nstages = n.  The HBM roofline of construction
+ * (bench.hpp:118-120 times it on the CPU). */
+typedef struct fpg_build_stage {
+    char name[24];
+    double ms;
+    double bytes;
+} fpg_build_stage;
+int fpg_dict_build_profile(const fpg_dict* dict, int32_t shard, fpg_build_stage* out, int32_t cap,
+                           int32_t* nstages);
 
 /* compute_frequencies (letter_model.hpp:33-45) on `device`: counts[256] of
  * the bytes (for select_letters over large corpora). */

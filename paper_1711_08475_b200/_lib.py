@@ -72,6 +72,8 @@ FPG_SIGNATURES = {
     "fpg_dict_size": (ctypes.c_int, [ctypes.c_void_p, c_u64p]),
     "fpg_dict_prints": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     "fpg_dict_build_seconds": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]),
+    "fpg_dict_build_profile": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32,
+                                              ctypes.POINTER(ctypes.c_int32)]),
     "fpg_build_fingerprints": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
                                               ctypes.POINTER(FpgScheme), ctypes.c_int32,
                                               ctypes.c_void_p]),
@@ -108,6 +110,10 @@ FPG_ABI_VERSION = 3  # include/fpg.h
 
 _fpg = None
 _corpus = None
+
+
+class FpgBuildStage(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 24), ("ms", ctypes.c_double), ("bytes", ctypes.c_double)]
 
 
 class FpgError(RuntimeError):

@@ -234,6 +234,32 @@ struct Collection {
     DBuf<uint32_t> hist;
     DBuf<uint8_t> cub_tmp;
     HBuf<uint32_t> h_hist;
+    // construction profile (dictionary collections): per stage, CUDA-event
+    // time on the build stream and algorithmic HBM bytes (reads + writes)
+    std::vector<fpg_build_stage> stages;
+    std::vector<cudaEvent_t> stage_ev;  // begin, end per stage (recorded around the launches only)
+    void stage_mark(cudaStream_t st) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        CK(cudaEventRecord(e, st));
+        stage_ev.push_back(e);
+    }
+    void stage_add(const char* name, double bytes) {  // after the stage's end mark
+        fpg_build_stage g{};
+        std::snprintf(g.name, sizeof(g.name), "%s", name);
+        g.bytes = bytes;
+        stages.push_back(g);
+    }
+    // after the build stream synchronised
+    void stage_finish() {
+        for (size_t i = 0; 2 * i + 1 < stage_ev.size() && i < stages.size(); ++i) {
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, stage_ev[2 * i], stage_ev[2 * i + 1]));
+            stages[i].ms = ms;
+        }
+        for (auto e : stage_ev) cudaEventDestroy(e);
+        stage_ev.clear();
+    }
 
     // Builds the bucketed layout of n strings already on the device.
     // Returns the number of kernel launches issued (ours, not CUB's).
@@ -257,12 +283,19 @@ struct Collection {
         }
         ids.reserve(n);
         len_b.reserve(n);
+        const bool prof = mode != kSliceQuery;
+        stages.clear();
         if (n) {
             len_a.reserve(n); idx_a.reserve(n); idx_b.reserve(n);
-            fpg::k_lengths<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(d_offs, n, len_a.p, idx_a.p, hist.p,
-                                                                   hist.p + L1);
+            if (prof) stage_mark(st);
+            fpg::k_lengths<<<(unsigned)std::min<uint64_t>(cdiv(n, 256), 148 * 8), 256, 0, st>>>(
+                d_offs, n, len_a.p, idx_a.p, hist.p, hist.p + L1);
             CK(cudaGetLastError());
             ++launches;
+            if (prof) {
+                stage_mark(st);
+                stage_add("k_lengths", 8.0 * (n + 1) + 6.0 * n);  // offsets in; lengths, identity ids out
+            }
         }
         CK(cudaMemcpyAsync(h_hist.p, hist.p, sizeof(uint32_t) * (L1 + 1), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
@@ -286,6 +319,11 @@ struct Collection {
         if (!n) return launches;
         int end_bit = 1;
         while ((1 << end_bit) <= max_len) ++end_bit;
+        uint64_t ends[2] = {0, 0};  // offsets[0], offsets[n]: the word bytes K1 reads
+        CK(cudaMemcpyAsync(&ends[0], d_offs, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&ends[1], d_offs + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const uint64_t blob_bytes = ends[1] - ends[0];
         size_t tmp = 0;
         const unsigned grid = (unsigned)cdiv(n, 256);
         if (mode == kSliceDict) {
@@ -294,6 +332,7 @@ struct Collection {
             // group-weight boxes
             wkey_a.reserve(n);
             wkey_b.reserve(n);
+            if (prof) stage_mark(st);
 #define FPG_KEYS(V) fpg::k_weight_keys<V><<<grid, 256, 0, st>>>(d_blob, d_offs, n, P, wkey_a.p)
             switch (P.variant) {
                 case 0: FPG_KEYS(0); break;
@@ -304,9 +343,15 @@ struct Collection {
 #undef FPG_KEYS
             CK(cudaGetLastError());
             ++launches;
+            if (prof) {
+                stage_mark(st);
+                // offsets and word bytes in, (length, group weights) keys out
+                stage_add("k_weight_keys", 8.0 * (n + 1) + (double)blob_bytes + 4.0 * n);
+            }
             CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, wkey_a.p, wkey_b.p, idx_a.p, idx_b.p, (int)n, 0,
                                                end_bit + 16, st));
             cub_tmp.reserve(tmp);
+            if (prof) stage_mark(st);
             CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, tmp, wkey_a.p, wkey_b.p, idx_a.p, idx_b.p, (int)n, 0,
                                                end_bit + 16, st));
             wt.reserve(n);
@@ -314,12 +359,20 @@ struct Collection {
             CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, len_a.p, len_b.p, idx_a.p, idx_b.p, (int)n, 0,
                                                end_bit, st));
             cub_tmp.reserve(tmp);
+            if (prof) stage_mark(st);
             CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, tmp, len_a.p, len_b.p, idx_a.p, idx_b.p, (int)n, 0,
                                                end_bit, st));
+        }
+        if (prof) {
+            stage_mark(st);
+            // CUB onesweep (library): one read + write of keys and values per 8-bit digit pass
+            const int passes = ((mode == kSliceDict ? end_bit + 16 : end_bit) + 7) / 8;
+            stage_add("cub_radix_sort", passes * 2.0 * (mode == kSliceDict ? 8.0 : 6.0) * n);
         }
         uint64_t* cmp_p = mode == kGenericDict ? cmp.p : nullptr;
         uint32_t* sig_p = mode == kGenericDict ? sig.p : nullptr;
         uint32_t* sigp_p = mode == kGenericDict ? nullptr : sigp.p;
+        if (prof) stage_mark(st);
 #define FPG_BUILD(V) fpg::k_build<V><<<grid, 256, 0, st>>>(d_blob, d_offs, idx_b.p, n, d_start.p, d_byte_base.p, P, \
                                                            fp.p, cmp_p, sig_p, sigp_p, ids.p, bytes.p, nullptr,    \
                                                            nullptr, nullptr, 0, mode == kSliceDict ? wt.p : nullptr)
@@ -332,6 +385,12 @@ struct Collection {
 #undef FPG_BUILD
         CK(cudaGetLastError());
         ++launches;
+        if (prof) {
+            stage_mark(st);
+            // order, offsets and word bytes in; fingerprints, codes, ids, padded bytes (and weights) out
+            const double out_w = mode == kSliceDict ? 8.0 + 4.0 + 4.0 + 4.0 : 8.0 + 8.0 + 4.0 + 4.0;
+            stage_add("k_build", 4.0 * n + 8.0 * (n + 1) + (double)blob_bytes + out_w * n + (double)total_bytes);
+        }
         // pre-check off: equal (zero) signatures pass every pair through
         if (mode == kGenericDict && !g_sig_precheck) CK(cudaMemsetAsync(sig.p, 0, n * sizeof(uint32_t), st));
         if (mode == kSliceDict) {
@@ -354,12 +413,18 @@ struct Collection {
             CK(cudaMemcpyAsync(d_count.p, count.data(), sizeof(uint32_t) * L1, cudaMemcpyHostToDevice, st));
             CK(cudaMemcpyAsync(d_plane_base.p, plane_base.data(), sizeof(uint64_t) * L1, cudaMemcpyHostToDevice, st));
             slab_w.reserve(sl);
-            fpg::k_planes<<<(unsigned)cdiv(sl * 32, 256), 256, 0, st>>>(fp.p, sigp.p, wt.p, slab_w.p,
+            if (prof) stage_mark(st);
+            fpg::k_planes<<<(unsigned)cdiv(sl, fpg::kPlanesSlabs), 32 * fpg::kPlanesSlabs, 0, st>>>(fp.p, sigp.p, wt.p, slab_w.p,
                                                                         d_slab_start.p, d_start.p,
                                                                         d_count.p, d_plane_base.p, L1, (uint32_t)sl,
                                                                         P.width, npt, planes.p);
             CK(cudaGetLastError());
             ++launches;
+            if (prof) {
+                stage_mark(st);
+                // fingerprints, codes, weights in; planes and slab boxes out
+                stage_add("k_planes", 16.0 * n + 4.0 * (double)pb + 8.0 * (double)sl);
+            }
         }
         return launches;
     }
@@ -1277,6 +1342,7 @@ void finish_dict(fpg_dict& D, const std::vector<unsigned long long>& hist, const
         sh.dict.build(sh.blob.p, sh.offs.p + offs_at[g], sh.n, D.params, sh.stream,
                       D.slice ? kSliceDict : kGenericDict, D.npt);
         CK(cudaStreamSynchronize(sh.stream));
+        sh.dict.stage_finish();
         sh.dict.drop_scratch();
         sh.blob.release();
         sh.offs.release();
@@ -1446,6 +1512,16 @@ int fpg_dict_build_seconds(const fpg_dict* dict, double* seconds) {
     return guarded([&] {
         if (!dict || !seconds) throw Error(FPG_EINVAL, "null argument");
         *seconds = dict->build_seconds;
+    });
+}
+
+int fpg_dict_build_profile(const fpg_dict* dict, int32_t shard, fpg_build_stage* out, int32_t cap, int32_t* nstages) {
+    return guarded([&] {
+        if (!dict || !nstages || (cap > 0 && !out)) throw Error(FPG_EINVAL, "null argument");
+        if (shard < 0 || shard >= (int32_t)dict->shards.size()) throw Error(FPG_EINVAL, "no such shard");
+        const auto& st = dict->shards[(size_t)shard]->dict.stages;
+        *nstages = (int32_t)st.size();
+        for (int32_t i = 0; i < cap && i < (int32_t)st.size(); ++i) out[i] = st[(size_t)i];
     });
 }
 

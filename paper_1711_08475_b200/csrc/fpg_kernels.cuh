@@ -288,17 +288,29 @@ __global__ void k_lengths(const uint64_t* __restrict__ offsets, uint64_t n,
     __shared__ uint32_t h[256];
     h[threadIdx.x] = 0;
     __syncthreads();
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) {
-        uint64_t len = offsets[i + 1] - offsets[i];
-        if (len > (uint64_t)kMaxLen) {
-            atomicAdd(too_long, 1u);
-            len = kMaxLen;
+    // grid-stride (a few CTAs per SM): the per-CTA flush of the shared
+    // histogram to its ~L global counters happens once per CTA, not per 256 words
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
+        const uint64_t i = i0 + threadIdx.x;
+        uint32_t key = 0xffffffffu;  // this thread's length (none past n)
+        if (i < n) {
+            uint64_t len = offsets[i + 1] - offsets[i];
+            if (len > (uint64_t)kMaxLen) {
+                atomicAdd(too_long, 1u);
+                len = kMaxLen;
+            }
+            len_out[i] = (uint16_t)len;
+            idx_out[i] = (uint32_t)i;
+            key = (uint32_t)len;
         }
-        len_out[i] = (uint16_t)len;
-        idx_out[i] = (uint32_t)i;
-        if (len < 256) atomicAdd(&h[len], 1u);
-        else atomicAdd(&hist[len], 1u);
+        // warp-aggregated: lanes with equal lengths add once (a dictionary has
+        // few distinct lengths, so per-thread shared atomics would serialise)
+        const uint32_t peers = __match_any_sync(0xffffffffu, key);
+        if (key != 0xffffffffu && (int)(threadIdx.x & 31) == __ffs(peers) - 1) {
+            if (key < 256) atomicAdd(&h[key], (uint32_t)__popc(peers));
+            else atomicAdd(&hist[key], (uint32_t)__popc(peers));
+        }
     }
     __syncthreads();
     if (h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);

@@ -597,53 +597,70 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
 
 // ---------------------------------------------------------------- K1b planes
 // One warp per slab: lane i holds word 32 s + i of its bucket; plane b is the
-// ballot of bit b of the words' codes (fingerprint bits, then sig' bits).
+// ballot of bit b of the words' codes (fingerprint bits, then sig' bits).  A
+// CTA of kPlanesSlabs warps handles that many consecutive global slabs and
+// stores each plane row through shared memory, so a row of consecutive slabs
+// leaves as one coalesced store instead of one 4-byte word per warp.
+constexpr int kPlanesSlabs = 32;  // warps (= consecutive slabs) per CTA
 #ifndef FPG_K2_TU  // defined once, in fpg_api.cu
-__global__ void k_planes(const uint64_t* __restrict__ fp, const uint32_t* __restrict__ sigp,
-                         const uint32_t* __restrict__ weight, uint2* __restrict__ slab_w,
-                         const uint32_t* __restrict__ slab_start,  // per length: first global slab (L1 + 1)
-                         const uint32_t* __restrict__ start,       // per length: first sorted position
-                         const uint32_t* __restrict__ count,       // per length: words
-                         const uint64_t* __restrict__ plane_base,  // per length: u32 offset of the planes
-                         int nlen, uint32_t total_slabs, int np, int npt, uint32_t* __restrict__ planes) {
-    const uint32_t gs = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (gs >= total_slabs) return;
-    int lo = 0, hi = nlen;  // largest L with slab_start[L] <= gs
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (slab_start[mid] <= gs) lo = mid;
-        else hi = mid;
+__global__ void __launch_bounds__(32 * kPlanesSlabs) k_planes(
+    const uint64_t* __restrict__ fp, const uint32_t* __restrict__ sigp, const uint32_t* __restrict__ weight,
+    uint2* __restrict__ slab_w,
+    const uint32_t* __restrict__ slab_start,  // per length: first global slab (L1 + 1)
+    const uint32_t* __restrict__ start,       // per length: first sorted position
+    const uint32_t* __restrict__ count,       // per length: words
+    const uint64_t* __restrict__ plane_base,  // per length: u32 offset of the planes
+    int nlen, uint32_t total_slabs, int np, int npt, uint32_t* __restrict__ planes) {
+    __shared__ uint32_t tile[96][kPlanesSlabs + 1];  // [plane][slab of the CTA]
+    __shared__ int s_l0;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t gs0 = blockIdx.x * kPlanesSlabs;
+    const uint32_t gs = gs0 + (uint32_t)w;
+    // bucket of the CTA's first slab (largest L with slab_start[L] <= gs0),
+    // searched once; the CTA's 32 slabs reach at most a few buckets further
+    if (threadIdx.x == 0) {
+        int lo = 0, hi = nlen;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (slab_start[mid] <= gs0) lo = mid;
+            else hi = mid;
+        }
+        s_l0 = lo;
     }
-    const int L = lo;
-    const uint32_t s = gs - slab_start[L];
-    const uint32_t ns = slab_start[L + 1] - slab_start[L];
-    const uint32_t w = 32u * s + lane;
-    const bool ok = w < count[L];
-    const uint64_t f = ok ? fp[start[L] + w] : 0ull;
-    const uint32_t g = ok ? sigp[start[L] + w] : 0u;
-    if (slab_w) {  // the slab's group-weight box (K2's weight window): per-byte min / max
-        const uint32_t wt = ok ? weight[start[L] + w] : 0u;
-        const uint2 box = warp_box(ok ? wt : 0xffffffffu, ok ? wt : 0u);
-        if (lane == 0) slab_w[gs] = box;
-    }
-    uint32_t mine[3] = {0u, 0u, 0u};
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-#pragma unroll
-        for (int t = 0; t < 32; ++t) {
-            const int b = 32 * r + t;
-            if (b < npt) {  // warp-uniform
-                const uint32_t bit = b < np ? (uint32_t)(f >> b) & 1u : (g >> (b - np)) & 1u;
-                const uint32_t ball = __ballot_sync(0xffffffffu, bit != 0);
-                if (lane == t) mine[r] = ball;
-            }
+    __syncthreads();
+    auto bucket = [&](uint32_t g) {
+        int L = s_l0;
+        while (slab_start[L + 1] <= g) ++L;
+        return L;
+    };
+    if (gs < total_slabs) {
+        const int L = bucket(gs);
+        const uint32_t s = gs - slab_start[L];
+        const uint32_t wi = 32u * s + lane;
+        const bool ok = wi < count[L];
+        const uint64_t f = ok ? fp[start[L] + wi] : 0ull;
+        const uint32_t g = ok ? sigp[start[L] + wi] : 0u;
+        if (slab_w) {  // the slab's group-weight box (K2's weight window): per-byte min / max
+            const uint32_t wt = ok ? weight[start[L] + wi] : 0u;
+            const uint2 box = warp_box(ok ? wt : 0xffffffffu, ok ? wt : 0u);
+            if (lane == 0) slab_w[gs] = box;
+        }
+        for (int b = 0; b < npt; ++b) {  // warp-uniform
+            const uint32_t bit = b < np ? (uint32_t)(f >> b) & 1u : (g >> (b - np)) & 1u;
+            const uint32_t ball = __ballot_sync(0xffffffffu, bit != 0);
+            if (lane == 0) tile[b][w] = ball;
         }
     }
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-        const int b = 32 * r + lane;
-        if (b < npt) planes[plane_base[L] + (uint64_t)b * ns + s] = mine[r];
+    __syncthreads();
+    // rows: element (b, slab gs0 + i), i = lane; consecutive lanes write
+    // consecutive slabs of one bucket's plane row
+    for (int b = w; b < npt; b += kPlanesSlabs) {
+        const uint32_t g = gs0 + (uint32_t)lane;
+        if (g < total_slabs) {
+            const int L = bucket(g);
+            const uint32_t ns = slab_start[L + 1] - slab_start[L];
+            planes[plane_base[L] + (uint64_t)b * ns + (g - slab_start[L])] = tile[b][lane];
+        }
     }
 }
 #endif

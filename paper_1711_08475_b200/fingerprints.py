@@ -526,6 +526,16 @@ class GpuFingerprintedDictionary:
         check(self._lib.fpg_dict_build_seconds(self._h, ctypes.byref(s)))
         return s.value
 
+    def build_profile(self, shard: int = 0) -> list[dict]:
+        """Construction stages of one shard: name, device ms (CUDA events)
+        and algorithmic HBM bytes (fpg_dict_build_profile)."""
+        from ._lib import FpgBuildStage
+
+        arr = (FpgBuildStage * 8)()
+        n = ctypes.c_int32()
+        check(self._lib.fpg_dict_build_profile(self._h, shard, arr, 8, ctypes.byref(n)))
+        return [{"name": arr[i].name.decode(), "ms": arr[i].ms, "bytes": arr[i].bytes} for i in range(min(n.value, 8))]
+
     # queries
     def query_batch(self, queries, opt: QueryOptions, per_query_stats: bool = False):
         """All queries in one GPU pass.  Returns (MatchCSR, stats[nq,5] | None)."""

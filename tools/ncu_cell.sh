@@ -9,6 +9,8 @@ echo ncu_rc=$?
 python tools/ncu_summary.py report $o/k_slice.ncu-rep 40 > $o/k_slice_summary.txt 2>&1
 python tools/ncu_summary.py sass $o/k_slice.ncu-rep > $o/k_slice_sass.txt 2>&1
 ncu -i $o/k_slice.ncu-rep --page source --csv --print-source sass 2>/dev/null | gzip > $o/k_slice_sass.csv.gz
+key=$(python -c "import bench; w=bench.Workload.__new__(bench.Workload); w.cfg, w.cell = $cfg, $cell; print('config$cfg', w.cell_name())")
+python tools/ncu_summary.py traffic $o/k_slice.ncu-rep "$key" $o/traffic.json > /dev/null 2>&1
 rm -f $o/k_slice.ncu-rep
 env "$@" timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $o/launches.csv \
   python bench.py --config $cfg --cell $cell --no-cpu-baseline --no-e2e --steps 1 --warmup 1 > $o/ncu_l.log 2>&1; echo ncu_l_rc=$?
