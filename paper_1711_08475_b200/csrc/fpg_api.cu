@@ -61,8 +61,9 @@ int guarded(F&& f) {
 
 inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 // per-run device counters: key slots reserved, survivors, tile counter, verifier
-// candidates, big segment flag, matches, pairs evaluated after the weight skip
-constexpr int kNumCounters = 7;
+// candidates, big segment flag, matches, pairs evaluated after the weight skip,
+// segments listed for k_seg_sort_big, its bucket overflow flag
+constexpr int kNumCounters = 9;
 constexpr unsigned kScatterBlocks = 148 * 4;  // grid-stride K4 scatter (the count is only known on the device)
 inline int stride_of(int len) { return len <= 16 ? 16 : (len + 15) & ~15; }
 
@@ -518,13 +519,13 @@ struct ShardBatch {
     std::vector<fpg::SliceTile> splan;
     bool plan_valid = false;
     std::vector<uint32_t> plan_qcount;  // query length histogram the plan was built for
-    bool seg_k4 = true;  // speculative segmented K4 (reset at upload)
     fpg_query_options plan_opts{};
     DBuf<unsigned long long> out;
     DBuf<unsigned long long> counters;  // [0] out_count, [1] survivors_total, [2] tile counter
     DBuf<uint32_t> qsurv;
     DBuf<uint64_t> offsets;
     DBuf<uint32_t> ids, ids2;
+    DBuf<uint32_t> big_list;  // K4: queries with more than kSegMax matches
     const uint32_t* ids_out = nullptr;  // sorted word ids of the last run (ids or ids2)
     DBuf<uint8_t> cub_tmp;
     HBuf<unsigned long long> h_counters;
@@ -902,9 +903,11 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
     }
     // K2, then K4 speculatively on the segmented path (no host round trip);
     // the one sync reads the counters and redoes what they rule out: a
-    // larger output buffer (rescan) or a query with > kSegMax matches (CUB sort).
+    // larger output buffer (rescan), or sorts the queries with > kSegMax
+    // matches (k_seg_sort_big).
     S.offsets.reserve(nq + 1);
-    const bool warp_sort = S.seg_k4 && nq;  // this run warp-sorts the segments (else CUB below)
+    S.big_list.reserve(nq);
+    const bool warp_sort = nq != 0;
     for (bool first = true;; first = false) {
         S.out.reserve(S.out_cap);
         S.ids.reserve(S.out.cap);
@@ -925,9 +928,8 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         }
         CK(cudaEventRecord(S.ev[2], st));
         // K4: offsets = exclusive scan of the per-query match counts, keys
-        // scattered into their query's segment, then each segment sorted by
-        // one warp (<= kSegMax matches).  Batches known to have larger
-        // segments skip the warp sort; the host sorts their segments below.
+        // scattered into their query's segment, then each segment of <=
+        // kSegMax matches sorted by one warp; larger ones are listed.
         if (nq) {  // accumulated in 64 bits: a batch may hold >= 2^32 matches
             size_t tmp = 0;
             CK(cub::DeviceScan::ExclusiveScan(nullptr, tmp, S.qsurv.p + nq, S.offsets.p, cuda::std::plus<>{}, uint64_t(0),
@@ -943,7 +945,8 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         S.launches += 2;
         if (warp_sort) {
             fpg::k_seg_sort<<<(unsigned)cdiv(nq * 32, 256), 256, 0, st>>>(S.offsets.p, nq, S.out.cap, S.ids.p,
-                                                                           S.counters.p + 4);
+                                                                           S.counters.p + 4, S.big_list.p,
+                                                                           S.counters.p + 7);
             CK(cudaGetLastError());
             ++S.launches;
         }
@@ -958,11 +961,21 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
     S.scanned = use_slice ? S.h_counters.p[6] : executed;
 
     S.ids_out = S.ids.p;
-    if (S.total && (!warp_sort || S.h_counters.p[4])) {
-        // some query has more than kSegMax matches: sort every segment (CUB
-        // segmented sort of the 32-bit word ids; later runs of this batch
-        // skip the warp sort)
-        S.seg_k4 = false;
+    bool cub_sort = false;
+    if (S.total && S.h_counters.p[4]) {
+        // queries with more than kSegMax matches: one CTA each sorts them in
+        // place (ids2 is its bucket scratch)
+        S.ids2.reserve(S.total);
+        const uint64_t nbig = S.h_counters.p[7];
+        fpg::k_seg_sort_big<<<(unsigned)std::min<uint64_t>(nbig, 148 * 8), fpg::kBigThreads, 0, st>>>(
+            S.offsets.p, S.big_list.p, nbig, S.ids.p, S.ids2.p, S.counters.p + 8);
+        CK(cudaGetLastError());
+        ++S.launches;
+        CK(cudaMemcpyAsync(S.h_counters.p + 8, S.counters.p + 8, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        cub_sort = S.h_counters.p[8] != 0;  // a bucket too large (very skewed ids): sort everything with CUB
+    }
+    if (S.total && cub_sort) {
         if (S.total >= (1ull << 31)) throw Error(FPG_EINVAL, "more than 2^31 - 1 matches in one shard's batch");
         S.ids2.reserve(S.total);
         size_t tmp = 0;
@@ -1078,7 +1091,6 @@ void upload(fpg_batch* B, const uint8_t* qbytes, const uint64_t* qoffsets, uint6
             S.plan_valid = false;
             S.plan_qcount = B->qcount;
         }
-        S.seg_k4 = true;
         Collection& Q = S.queries;
         Q.n = nq;
         Q.count = B->qcount;

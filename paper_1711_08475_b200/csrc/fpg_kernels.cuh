@@ -421,16 +421,21 @@ __global__ void k_seg_scatter(const unsigned long long* __restrict__ keys, const
 #endif
 
 // One warp per query: bitonic sort of its <= 32 word ids in registers.
+// Larger segments are listed for k_seg_sort_big.
 #ifndef FPG_K2_TU  // defined once, in fpg_api.cu
 __global__ void k_seg_sort(const uint64_t* __restrict__ offsets, uint64_t nq, uint64_t cap, uint32_t* __restrict__ ids,
-                           unsigned long long* __restrict__ big_seg) {
+                           unsigned long long* __restrict__ big_seg, uint32_t* __restrict__ big_list,
+                           unsigned long long* __restrict__ n_big) {
     const uint64_t q = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (q >= nq) return;
     const uint64_t o = offsets[q];
     const uint64_t e = offsets[q + 1];
-    if (e - o > kSegMax) {  // large segment: the host sorts all segments (CUB)
-        if (lane == 0) *big_seg = 1ull;
+    if (e - o > kSegMax) {  // large segment: k_seg_sort_big (launched by the host after the run's sync)
+        if (lane == 0 && e <= cap) {
+            *big_seg = 1ull;
+            big_list[atomicAdd(n_big, 1ull)] = (uint32_t)q;
+        }
         return;
     }
     if (e > cap) return;  // overflowed run: the host reruns
@@ -448,6 +453,138 @@ __global__ void k_seg_sort(const uint64_t* __restrict__ offsets, uint64_t nq, ui
         }
     }
     if (lane < n) ids[o + lane] = v;
+}
+#endif
+
+// Segments of more than kSegMax ids (k_seg_sort's list), one CTA each, sorted
+// in place: the ids go to B buckets of equal value range over [min, max] of
+// the segment (B ~ n / 16, a power of two; tmp holds them bucket by bucket),
+// then the warps sort the buckets, <= 32 ids in registers (shuffle bitonic),
+// up to kBucketMax in shared memory, and write them back in bucket order.  A
+// bucket above kBucketMax ids (very skewed ids) sets *overflow: the host then
+// sorts every segment with CUB.
+constexpr int kBigThreads = 256;
+constexpr int kMaxBuckets = 2048;
+constexpr int kBucketMax = 512;
+#ifndef FPG_K2_TU  // defined once, in fpg_api.cu
+// ascending shared-memory bitonic sort of v[0, P), P a power of two, by one warp
+__device__ __forceinline__ void warp_smem_bitonic(uint32_t* v, int P, int lane) {
+    for (int k = 2; k <= P; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = lane; i < P / 2; i += 32) {
+                const int a = ((i & ~(j - 1)) << 1) | (i & (j - 1)), b = a | j;  // j is a power of two
+                const uint32_t x = v[a], y = v[b];
+                if ((x > y) == ((a & k) == 0)) {
+                    v[a] = y;
+                    v[b] = x;
+                }
+            }
+            __syncwarp();
+        }
+}
+// ascending bitonic sort of one value per lane (lanes past the data hold ~0)
+__device__ __forceinline__ uint32_t warp_reg_bitonic(uint32_t v, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const uint32_t u = __shfl_xor_sync(0xffffffffu, v, j);
+            const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+            v = (lower == up) ? min(v, u) : max(v, u);
+        }
+    return v;
+}
+
+__global__ void __launch_bounds__(kBigThreads) k_seg_sort_big(const uint64_t* __restrict__ offsets,
+                                                              const uint32_t* __restrict__ big_list, uint64_t n_big,
+                                                              uint32_t* __restrict__ ids, uint32_t* __restrict__ tmp,
+                                                              unsigned long long* __restrict__ overflow) {
+    constexpr int NW = kBigThreads / 32;
+    __shared__ uint32_t s_cnt[kMaxBuckets], s_cur[kMaxBuckets];
+    __shared__ uint32_t s_wv[NW][kBucketMax];
+    __shared__ uint32_t s_lo, s_hi, s_over;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (uint64_t bi = blockIdx.x; bi < n_big; bi += gridDim.x) {
+        const uint32_t q = big_list[bi];
+        const uint64_t o = offsets[q];
+        const int n = (int)(offsets[q + 1] - o);
+        uint32_t* seg = ids + o;
+        int B = 32;
+        while (B < n / 16 && B < kMaxBuckets) B <<= 1;
+        if (tid == 0) {
+            s_lo = 0xffffffffu;
+            s_hi = 0u;
+            s_over = 0u;
+        }
+        for (int i = tid; i < B; i += kBigThreads) s_cnt[i] = 0u;
+        uint32_t lo = 0xffffffffu, hi = 0u;
+        for (int i = tid; i < n; i += kBigThreads) {
+            const uint32_t v = seg[i];
+            lo = min(lo, v);
+            hi = max(hi, v);
+        }
+        lo = __reduce_min_sync(0xffffffffu, lo);
+        hi = __reduce_max_sync(0xffffffffu, hi);
+        __syncthreads();
+        if (lane == 0) {
+            atomicMin(&s_lo, lo);
+            atomicMax(&s_hi, hi);
+        }
+        __syncthreads();
+        lo = s_lo;
+        const uint64_t span = (uint64_t)s_hi - lo + 1;
+        auto bucket = [&](uint32_t v) { return (int)(((uint64_t)(v - lo) * (uint64_t)B) / span); };
+        for (int i = tid; i < n; i += kBigThreads) atomicAdd(&s_cnt[bucket(seg[i])], 1u);
+        __syncthreads();
+        // exclusive scan of the bucket counts (one warp)
+        if (warp == 0) {
+            uint32_t run = 0;
+            for (int b0 = 0; b0 < B; b0 += 32) {
+                const uint32_t c = s_cnt[b0 + lane];
+                if (c > (uint32_t)kBucketMax) s_over = 1u;
+                uint32_t incl = c;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (lane >= d) incl += v;
+                }
+                s_cur[b0 + lane] = run + incl - c;
+                run += __shfl_sync(0xffffffffu, incl, 31);
+            }
+        }
+        __syncthreads();
+        if (s_over) {  // left to the host's CUB fallback
+            if (tid == 0) *overflow = 1ull;
+            __syncthreads();
+            continue;
+        }
+        for (int i = tid; i < n; i += kBigThreads) {
+            const uint32_t v = seg[i];
+            tmp[o + atomicAdd(&s_cur[bucket(v)], 1u)] = v;
+        }
+        __syncthreads();
+        // s_cur[b] is now the end of bucket b; its start is s_cur[b] - s_cnt[b]
+        for (int b = warp; b < B; b += NW) {
+            const int c = (int)s_cnt[b];
+            if (!c) continue;
+            const uint32_t st = s_cur[b] - (uint32_t)c;
+            if (c <= 32) {
+                uint32_t v = lane < c ? tmp[o + st + lane] : 0xffffffffu;
+                v = warp_reg_bitonic(v, lane);
+                if (lane < c) seg[st + lane] = v;
+            } else {
+                int P = 64;
+                while (P < c) P <<= 1;
+                uint32_t* wv = s_wv[warp];
+                for (int i = lane; i < P; i += 32) wv[i] = i < c ? tmp[o + st + i] : 0xffffffffu;
+                __syncwarp();
+                warp_smem_bitonic(wv, P, lane);
+                for (int i = lane; i < c; i += 32) seg[st + i] = wv[i];
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+    }
 }
 #endif
 

@@ -270,6 +270,34 @@ def test_output_regrowth_many_matches(oracle):
     assert_same(csr, st, *oracle.query_batch(blob, offs, qblob, qoffs, osch(s), Metric.Levenshtein, 1, True, True))
 
 
+def test_k4_segment_size_classes(oracle):
+    """K4 sorts each query's matches by word id in one of three ways: <= 32
+    (warp bitonic), 33..4096 (one CTA, shared-memory bitonic) and larger
+    (value-range buckets, per-warp sorts), with a CUB fallback when one bucket
+    overflows.  The dictionary mixes duplicate runs so that one query hits
+    each class, and its ids are placed so the last query's bucket overflows."""
+    rng = np.random.default_rng(11)
+    words = [bytes(rng.integers(97, 123, size=int(rng.integers(3, 9)), dtype=np.uint8)) for _ in range(60_000)]
+    # 20 / 900 / 9000 copies at random (disjoint) ids past the first 3000
+    at = rng.permutation(np.arange(3000, len(words) - 1))
+    for w, (lo, hi) in [(b"qq", (0, 20)), (b"zx", (20, 920)), (b"kj", (920, 9920))]:
+        for i in at[lo:hi]:
+            words[int(i)] = w
+    # skew: 3000 copies of "vw" packed at the front, one at the very end
+    words[:3000] = [b"vw"] * 3000
+    words[-1] = b"vw"
+    blob, offs = pack(words)
+    qblob, qoffs = pack([b"qq", b"zx", b"kj", b"vw", b"ab"])
+    s = make_scheme(blob, Variant.Occurrence, 16)
+    for metric in (Metric.Hamming, Metric.Levenshtein):
+        with GpuFingerprintedDictionary((blob, offs), s) as d:
+            csr, st = d.query_batch((qblob, qoffs), QueryOptions(metric, 1, True, True), True)
+        counts = np.diff(csr.offsets)
+        if metric == Metric.Hamming:  # one query per size class
+            assert counts[0] <= 32 < counts[1] <= 4096 < counts[2] and counts[3] > 3000
+        assert_same(csr, st, *oracle.query_batch(blob, offs, qblob, qoffs, osch(s), metric, 1, True, True))
+
+
 def test_staged_batch_reruns_across_options(oracle):
     """One upload, several runs (fpg_batch_run) with options whose outputs
     differ in size and shape: the cached tile plan and the K4 path choice
