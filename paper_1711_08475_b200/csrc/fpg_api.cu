@@ -62,8 +62,9 @@ int guarded(F&& f) {
 inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 // per-run device counters: key slots reserved, survivors, tile counter, verifier
 // candidates, big segment flag, matches, pairs evaluated after the weight skip,
-// segments listed for k_seg_sort_big, its bucket overflow flag
-constexpr int kNumCounters = 9;
+// segments listed for k_seg_sort_big, its bucket overflow flag, the exact
+// path's tile counter and its pairs evaluated
+constexpr int kNumCounters = 11;
 constexpr unsigned kScatterBlocks = 148 * 4;  // grid-stride K4 scatter (the count is only known on the device)
 inline int stride_of(int len) { return len <= 16 ? 16 : (len + 15) & ~15; }
 
@@ -225,6 +226,10 @@ struct Collection {
     std::vector<uint64_t> plane_base;    // L1
     DBuf<uint32_t> planes;
     DBuf<uint32_t> wt;        // bit-sliced K2: group weights (fp_gweight) per sorted position
+    DBuf<uint32_t> xc;        // exact path: symbol codes of the first kXLen bytes (kXBits each)
+    DBuf<uint32_t> xplanes;   // exact path planes of the buckets L <= kXLen: fingerprint bits, then codes
+    std::vector<uint64_t> xplane_base;  // per length <= kXLen: u32 offset in xplanes
+    DBuf<uint64_t> d_xplane_base;
     DBuf<uint2> slab_w;       // bit-sliced dictionary: group-weight box (min, max bytes) per global slab
     DBuf<uint32_t> wkey_a, wkey_b;  // scratch: (length << 16 | group weights) sort keys
     DBuf<uint32_t> d_slab_start, d_count;
@@ -374,9 +379,14 @@ struct Collection {
         uint32_t* sig_p = mode == kGenericDict ? sig.p : nullptr;
         uint32_t* sigp_p = mode == kGenericDict ? nullptr : sigp.p;
         if (prof) stage_mark(st);
+        uint32_t* xc_p = nullptr;
+        if (mode == kSliceDict && P.xlen) {
+            xc.reserve(n);
+            xc_p = xc.p;
+        }
 #define FPG_BUILD(V) fpg::k_build<V><<<grid, 256, 0, st>>>(d_blob, d_offs, idx_b.p, n, d_start.p, d_byte_base.p, P, \
                                                            fp.p, cmp_p, sig_p, sigp_p, ids.p, bytes.p, nullptr,    \
-                                                           nullptr, nullptr, 0, mode == kSliceDict ? wt.p : nullptr)
+                                                           nullptr, nullptr, 0, mode == kSliceDict ? wt.p : nullptr, xc_p)
         switch (P.variant) {
             case 0: FPG_BUILD(0); break;
             case 1: FPG_BUILD(1); break;
@@ -426,6 +436,29 @@ struct Collection {
                 // fingerprints, codes, weights in; planes and slab boxes out
                 stage_add("k_planes", 16.0 * n + 4.0 * (double)pb + 8.0 * (double)sl);
             }
+            if (P.xlen) {
+                // exact path planes (same kernel): fingerprint bits, then the
+                // position codes, for the buckets of words <= kXLen bytes
+                const int xnpt = P.width + fpg::kXBits * fpg::kXLen;
+                xplane_base.assign(fpg::kXLen + 1, 0);
+                uint64_t xb = 0;
+                for (int L = 0; L <= fpg::kXLen; ++L) {
+                    xplane_base[L] = xb;
+                    xb += cdiv(count[L], 32) * (uint64_t)xnpt;
+                }
+                const uint32_t xsl = slab_start[fpg::kXLen + 1];
+                if (xsl) {
+                    xplanes.reserve(xb);
+                    d_xplane_base.reserve(fpg::kXLen + 1);
+                    CK(cudaMemcpyAsync(d_xplane_base.p, xplane_base.data(), sizeof(uint64_t) * (fpg::kXLen + 1),
+                                       cudaMemcpyHostToDevice, st));
+                    fpg::k_planes<<<(unsigned)cdiv(xsl, fpg::kPlanesSlabs), 32 * fpg::kPlanesSlabs, 0, st>>>(
+                        fp.p, xc.p, nullptr, nullptr, d_slab_start.p, d_start.p, d_count.p, d_xplane_base.p,
+                        fpg::kXLen + 1, xsl, P.width, xnpt, xplanes.p);
+                    CK(cudaGetLastError());
+                    ++launches;
+                }
+            }
         }
         return launches;
     }
@@ -455,14 +488,19 @@ struct Collection {
         uint32_t* sig_p = mode == kGenericDict ? sig.p : nullptr;
         uint32_t* sigp_p = mode == kGenericDict ? nullptr : sigp.p;
         uint32_t* wt_p = nullptr;
+        uint32_t* xc_p = nullptr;
         if (mode == kSliceQuery) {
             wt.reserve(n);
             wt_p = wt.p;
+            if (P.xlen) {
+                xc.reserve(n);
+                xc_p = xc.p;
+            }
         }
         const unsigned grid = (unsigned)std::max<uint64_t>(1, cdiv(n, 256));
 #define FPG_BUILD(V) fpg::k_build<V><<<grid, 256, 0, st>>>(d_blob, d_offs, d_order, n, d_start.p, d_byte_base.p, P, \
                                                            fp.p, cmp_p, sig_p, sigp_p, ids.p, bytes.p, len_b.p,  \
-                                                           zero_by_id, zero64, nzero64, wt_p)
+                                                           zero_by_id, zero64, nzero64, wt_p, xc_p)
         switch (P.variant) {
             case 0: FPG_BUILD(0); break;
             case 1: FPG_BUILD(1); break;
@@ -514,9 +552,9 @@ struct ShardBatch {
     DBuf<uint32_t> qorder;
     Collection queries;
     DBuf<fpg::Tile> tiles;
-    DBuf<fpg::SliceTile> stiles;
+    DBuf<fpg::SliceTile> stiles, stiles_x;
     std::vector<fpg::Tile> plan;
-    std::vector<fpg::SliceTile> splan;
+    std::vector<fpg::SliceTile> splan, splan_x;  // bit-sliced tiles; those of the exact path
     bool plan_valid = false;
     std::vector<uint32_t> plan_qcount;  // query length histogram the plan was built for
     fpg_query_options plan_opts{};
@@ -532,7 +570,7 @@ struct ShardBatch {
     HBuf<uint64_t> h_offsets;
     HBuf<uint32_t> h_ids, h_qsurv;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-    uint64_t total = 0, executed = 0, survivors = 0, candidates = 0, scanned = 0, launches = 0;
+    uint64_t total = 0, executed = 0, survivors = 0, candidates = 0, scanned = 0, scanned_x = 0, launches = 0;
     double run_ms = 0, filter_ms = 0;
     uint64_t out_cap = 1 << 20;
 };
@@ -680,6 +718,11 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
     uint64_t executed = 0;
     std::vector<fpg::Tile>& plan = S.plan;
     std::vector<fpg::SliceTile>& splan = S.splan;
+    std::vector<fpg::SliceTile>& splan_x = S.splan_x;
+    // exact Hamming path for the words of <= kXLen bytes (fpg_slice.cuh, X)
+    static const bool exact_on = env_double("FPG_EXACT", 1.0) != 0.0;
+    const bool xpath = exact_on && D->params.xlen && o.metric == FPG_HAMMING && o.k <= 1 && !o.exhaustive &&
+                       o.use_filter;
     // The tile plan depends only on the batch's length histogram and the
     // options: it is built (and uploaded) once and reused by later runs and
     // by later batches with the same histogram.
@@ -692,6 +735,7 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         executed = S.executed;
     } else if (use_slice) {
         splan.clear();
+        splan_x.clear();
         // Tile plan: per word length lw, the compatible query lengths form one
         // contiguous range of the length-sorted queries (Hamming / k = 0:
         // lw; Levenshtein k = 1: lw - 1 .. lw + 1, edit_distance.hpp:38-39).
@@ -754,7 +798,9 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
                     t.w_stride = (uint16_t)stride_of(lw);
                     t.count_only = count_only ? 1u : 0u;
                     t.slab_g0 = W.slab_start[lw];
-                    splan.push_back(t);
+                    const bool xt = xpath && lw <= fpg::kXLen && !count_only;
+                    if (xt) t.plane_base = W.xplane_base[lw];
+                    (xt ? splan_x : splan).push_back(t);
                 }
         };
         for (int lw = 0; lw <= W.max_len; ++lw) {
@@ -776,34 +822,38 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         // (small tiles cost a slab-group load per few queries: config 5 has
         // ~6e5 tiles and needs no cutting before its very end).
         auto cost = [](const fpg::SliceTile& x) { return (uint64_t)x.q_count * x.n_slabs; };
-        std::stable_sort(splan.begin(), splan.end(),
-                         [&](const fpg::SliceTile& x, const fpg::SliceTile& y) { return cost(x) > cost(y); });
-        uint64_t work = 0, acc = 0;
-        for (const auto& t : splan) work += cost(t);
-        std::vector<fpg::SliceTile> fine;
-        fine.reserve(splan.size() + splan.size() / 2);
         static const double env_a = env_double("FPG_TAIL_A", 0.35), env_b = env_double("FPG_TAIL_B", 0.85);
-        const double tail_f = std::min(1.0, 4.0 * 2 * sms / std::max<double>(1.0, (double)splan.size()));
-        const double tail_a = 1.0 - (1.0 - env_a) * tail_f, tail_b = 1.0 - (1.0 - env_b) * tail_f;
-        for (const auto& t : splan) {
-            acc += cost(t);
-            const uint32_t sub = acc <= tail_a * work ? t.q_count : acc <= tail_b * work ? 32u : 16u;
-            if (t.q_count <= sub) {
-                fine.push_back(t);
-                continue;
+        // each plan (one K2 launch) sorted largest first, its tail cut finer
+        auto finish_plan = [&](std::vector<fpg::SliceTile>& pl, DBuf<fpg::SliceTile>& dev) {
+            std::stable_sort(pl.begin(), pl.end(),
+                             [&](const fpg::SliceTile& x, const fpg::SliceTile& y) { return cost(x) > cost(y); });
+            uint64_t work = 0, acc = 0;
+            for (const auto& t : pl) work += cost(t);
+            std::vector<fpg::SliceTile> fine;
+            fine.reserve(pl.size() + pl.size() / 2);
+            const double tail_f = std::min(1.0, 4.0 * 2 * sms / std::max<double>(1.0, (double)pl.size()));
+            const double tail_a = 1.0 - (1.0 - env_a) * tail_f, tail_b = 1.0 - (1.0 - env_b) * tail_f;
+            for (const auto& t : pl) {
+                acc += cost(t);
+                const uint32_t sub = acc <= tail_a * work ? t.q_count : acc <= tail_b * work ? 32u : 16u;
+                if (t.q_count <= sub) {
+                    fine.push_back(t);
+                    continue;
+                }
+                for (uint32_t q0 = 0; q0 < t.q_count; q0 += sub) {
+                    fpg::SliceTile u = t;
+                    u.q_begin = t.q_begin + q0;
+                    u.q_count = std::min<uint32_t>(sub, t.q_count - q0);
+                    fine.push_back(u);
+                }
             }
-            for (uint32_t q0 = 0; q0 < t.q_count; q0 += sub) {
-                fpg::SliceTile u = t;
-                u.q_begin = t.q_begin + q0;
-                u.q_count = std::min<uint32_t>(sub, t.q_count - q0);
-                fine.push_back(u);
-            }
-        }
-        splan.swap(fine);
-        S.stiles.reserve(splan.size());
-        if (!splan.empty())
-            CK(cudaMemcpyAsync(S.stiles.p, splan.data(), splan.size() * sizeof(fpg::SliceTile),
-                               cudaMemcpyHostToDevice, st));
+            pl.swap(fine);
+            dev.reserve(pl.size());
+            if (!pl.empty())
+                CK(cudaMemcpyAsync(dev.p, pl.data(), pl.size() * sizeof(fpg::SliceTile), cudaMemcpyHostToDevice, st));
+        };
+        finish_plan(splan, S.stiles);
+        finish_plan(splan_x, S.stiles_x);
     } else {
         // Generic k_scan: one tile per (query length, word length) bucket pair block.
         plan.clear();
@@ -921,6 +971,18 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         if (use_slice && !splan.empty()) {
             dispatch_slice(D->scheme, D->params.nsig, S.stiles.p, (uint32_t)splan.size(), SP, st, sh.device);
             ++S.launches;
+        }
+        if (use_slice && !splan_x.empty()) {
+            // the exact path: position-code planes instead of sig', own tile
+            // counter and pair count
+            fpg::SliceParams SX = SP;
+            SX.planes = W.xplanes.p;
+            SX.q_sigp = Q.xc.p;
+            SX.tile_counter = reinterpret_cast<unsigned int*>(S.counters.p + 9);
+            SX.scanned = S.counters.p + 10;
+            fpg_host::dispatch_slice_16x(field_width_of(D->scheme), S.stiles_x.p, (uint32_t)splan_x.size(), SX, st,
+                                         sh.device);
+            ++S.launches;
         } else if (!use_slice && !plan.empty()) {
             dispatch_scan(D->params, D->params.onehot && !from_slice, o.want_stats != 0, S.tiles.p,
                           (uint32_t)plan.size(), P, st, sh.device);
@@ -958,7 +1020,8 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
     S.total = S.h_counters.p[5];
     S.survivors = S.h_counters.p[1];
     S.candidates = S.h_counters.p[3];
-    S.scanned = use_slice ? S.h_counters.p[6] : executed;
+    S.scanned = use_slice ? S.h_counters.p[6] + S.h_counters.p[10] : executed;
+    S.scanned_x = use_slice ? S.h_counters.p[10] : 0;
 
     S.ids_out = S.ids.p;
     bool cub_sort = false;
@@ -1248,6 +1311,19 @@ void configure_slice(fpg_dict& D, const std::vector<unsigned long long>& hist) {
         for (size_t r = 0; r < others.size(); ++r) D.params.sigbit[others[r]] = (int8_t)(r % S);
     D.params.nsig = S;
     D.npt = D.scheme.width + S;
+    // exact Hamming path of short words (K2 X, fpg_slice.cuh): W = 16 and at
+    // most 31 distinct dictionary bytes, coded densely in kXBits bits; bytes
+    // the dictionary lacks share code 31, which no dictionary word uses
+    int distinct = 0;
+    for (int c = 0; c < 256; ++c) distinct += hist[c] ? 1 : 0;
+    std::memset(D.params.xcode, (1 << fpg::kXBits) - 1, sizeof(D.params.xcode));
+    D.params.xlen = 0;
+    if (D.slice && D.scheme.width == 16 && distinct < (1 << fpg::kXBits)) {
+        int r = 0;
+        for (int c = 0; c < 256; ++c)
+            if (hist[c]) D.params.xcode[c] = (uint8_t)r++;
+        D.params.xlen = fpg::kXLen;
+    }
 }
 
 void make_batch(fpg_dict* D, fpg_batch** out) {
@@ -1722,6 +1798,13 @@ int fpg_batch_last_scanned(const fpg_batch* batch, int32_t shard, uint64_t* scan
     return guarded([&] {
         if (!batch || !scanned || shard < 0 || (size_t)shard >= batch->sb.size()) throw Error(FPG_EINVAL, "bad shard");
         *scanned = batch->sb[(size_t)shard]->scanned;
+    });
+}
+
+int fpg_batch_last_scanned_exact(const fpg_batch* batch, int32_t shard, uint64_t* scanned) {
+    return guarded([&] {
+        if (!batch || !scanned || shard < 0 || (size_t)shard >= batch->sb.size()) throw Error(FPG_EINVAL, "bad shard");
+        *scanned = batch->sb[(size_t)shard]->scanned_x;
     });
 }
 

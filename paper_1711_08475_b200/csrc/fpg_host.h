@@ -41,6 +41,9 @@ void dispatch_slice_32(int fw, int nsig, const fpg::SliceTile* tiles, uint32_t n
                        cudaStream_t st, int device);
 void dispatch_slice_64(int fw, int nsig, const fpg::SliceTile* tiles, uint32_t ntiles, const fpg::SliceParams& P,
                        cudaStream_t st, int device);
+// exact Hamming path of words <= kXLen bytes, W = 16 (fpg_k2_slice_w16.cu)
+void dispatch_slice_16x(int fw, const fpg::SliceTile* tiles, uint32_t ntiles, const fpg::SliceParams& P,
+                        cudaStream_t st, int device);
 // K2 generic (fpg_k2_scan.cu): k_scan<kind, W, stats>.
 void dispatch_scan(int kind, int width, bool stats, const fpg::Tile* tiles, uint32_t ntiles,
                    const fpg::ScanParams& P, cudaStream_t st, int device);

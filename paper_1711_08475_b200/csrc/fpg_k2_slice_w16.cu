@@ -7,14 +7,15 @@
 namespace fpg_host {
 namespace {
 
-template <int NP, int FW, int EXTRA, int S>
+template <int NP, int FW, int EXTRA, int S, bool X = false>
 void launch_slice(const fpg::SliceTile* tiles, uint32_t ntiles, const fpg::SliceParams& P, cudaStream_t st,
                   int device) {
     // the common options (filter + stats + window on, k = 1) run the HOT instantiation
     const bool hot = P.use_fp && P.stats && P.wskip && !P.exhaustive && P.k == 1;
-    auto kern = hot ? fpg::k_slice<NP, FW, EXTRA, S, true> : fpg::k_slice<NP, FW, EXTRA, S, false>;
+    auto kern = hot ? fpg::k_slice<NP, FW, EXTRA, S, true, X> : fpg::k_slice<NP, FW, EXTRA, S, false, X>;
     constexpr size_t smem = fpg::slice_smem_bytes(NP + S);
     static int resident[2][64] = {{0}};  // per variant and device: CTAs resident on the whole GPU (0 = not queried)
+    (void)X;
     const int dv = device & 63;
     if (!resident[hot][dv]) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -49,6 +50,18 @@ void dispatch_slice_16(int fw, int nsig, const fpg::SliceTile* tiles, uint32_t n
         case 2: launch_slice_s<16, 2, 0>(nsig, tiles, ntiles, P, st, device); break;
         case 3: launch_slice_s<16, 3, 16 % 3>(nsig, tiles, ntiles, P, st, device); break;
         default: launch_slice_s<16, 4, 0>(nsig, tiles, ntiles, P, st, device); break;
+    }
+}
+
+// The exact Hamming path of short words (k_slice<16, fw, extra, kXBits * kXLen, *, X = true>).
+void dispatch_slice_16x(int fw, const fpg::SliceTile* tiles, uint32_t ntiles, const fpg::SliceParams& P,
+                        cudaStream_t st, int device) {
+    constexpr int SX = fpg::kXBits * fpg::kXLen;
+    switch (fw) {
+        case 1: launch_slice<16, 1, 0, SX, true>(tiles, ntiles, P, st, device); break;
+        case 2: launch_slice<16, 2, 0, SX, true>(tiles, ntiles, P, st, device); break;
+        case 3: launch_slice<16, 3, 16 % 3, SX, true>(tiles, ntiles, P, st, device); break;
+        default: launch_slice<16, 4, 0, SX, true>(tiles, ntiles, P, st, device); break;
     }
 }
 

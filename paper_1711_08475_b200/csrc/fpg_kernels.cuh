@@ -23,6 +23,10 @@
 namespace fpg {
 
 constexpr int kMaxLen = 4096;
+// Words of at most kXLen bytes get exact position-code planes (K2's exact
+// Hamming path, fpg_slice.cuh): 5 bits per position.
+constexpr int kXLen = 4;
+constexpr int kXBits = 5;
 
 // Symbol -> slot table and scheme constants.  Passed by value as a kernel
 // parameter, i.e. it lives in the constant bank; K1 copies the table into
@@ -30,6 +34,8 @@ constexpr int kMaxLen = 4096;
 struct SchemeParams {
     int8_t slot[256];
     int8_t sigbit[256];    // sig' field of a non-letter byte (fpg_slice.cuh), or -1
+    uint8_t xcode[256];    // exact path: dense code of a dictionary byte (< 31); 31 for bytes the dictionary lacks
+    int32_t xlen;          // exact path on (kXLen) or off (0)
     int32_t nsig;          // sig' fields S
     int32_t variant, width, b, p, nletters, slots, extra;
     int32_t onehot;        // count, W=16, b=2: K2 compares a 32-bit one-hot form
@@ -232,11 +238,14 @@ __global__ void __launch_bounds__(256) k_build(const uint8_t* __restrict__ blob,
                                                uint16_t* __restrict__ len_out = nullptr,
                                                uint32_t* __restrict__ zero_by_id = nullptr,
                                                unsigned long long* __restrict__ zero64 = nullptr,
-                                               int nzero64 = 0, uint32_t* __restrict__ weight_out = nullptr) {
+                                               int nzero64 = 0, uint32_t* __restrict__ weight_out = nullptr,
+                                               uint32_t* __restrict__ xc_out = nullptr) {
     __shared__ int8_t s_slot[256];
     __shared__ int8_t s_sigbit[256];
+    __shared__ uint8_t s_xcode[256];
     s_slot[threadIdx.x] = P.slot[threadIdx.x];           // blockDim == 256
     s_sigbit[threadIdx.x] = P.sigbit[threadIdx.x];
+    s_xcode[threadIdx.x] = P.xcode[threadIdx.x];
     __syncthreads();
     if (zero64 && blockIdx.x == 0 && (int)threadIdx.x < nzero64) zero64[threadIdx.x] = 0ull;
     const uint64_t pos = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -250,7 +259,7 @@ __global__ void __launch_bounds__(256) k_build(const uint8_t* __restrict__ blob,
     uint8_t* dst = bytes_out ? bytes_out + bucket_bytes[len] + (uint64_t)(pos - bucket_start[len]) * stride : nullptr;
     FpBuilder<VARIANT> fb;
     fb.init(P);
-    uint32_t sig = 0, sigp = 0;
+    uint32_t sig = 0, sigp = 0, xc = 0;  // xc: position codes of the first kXLen bytes (exact path)
     for (int c = 0; c < stride; c += 16) {
         uint32_t w[4];
         const int rem = min(16, len - c);
@@ -266,6 +275,7 @@ __global__ void __launch_bounds__(256) k_build(const uint8_t* __restrict__ blob,
                 sig |= 1u << (byte & 31);
                 const int g = s_sigbit[byte];
                 if (g >= 0) sigp |= 1u << g;
+                if (c + t < kXLen) xc |= (uint32_t)s_xcode[byte] << (kXBits * (c + t));
             }
         }
     }
@@ -276,6 +286,7 @@ __global__ void __launch_bounds__(256) k_build(const uint8_t* __restrict__ blob,
     if (sigp_out) sigp_out[pos] = sigp;
     if (id_out) id_out[pos] = id;
     if (weight_out) weight_out[pos] = fp_gweight(fp, P);
+    if (xc_out) xc_out[pos] = xc;
 }
 
 // Lengths, identity ids and the length histogram (lengths < 256 counted in

@@ -179,7 +179,14 @@ __host__ __device__ constexpr size_t slice_smem_bytes(int npt) {
 // filter on, QueryStats on, weight window on, k = 1, not exhaustive), so the
 // per-step code carries no uniform branches on them; other runs take the
 // generic instantiation (HOT = false), which reads them from P.
-template <int NP, int FW, int EXTRA, int S, bool HOT>
+//
+// X (exact Hamming path, words of <= kXLen bytes): planes NP.. are not sig'
+// but the words' symbol codes, kXBits planes per byte position, and q_sigp
+// holds the queries' codes.  After the scheme fields (QueryStats) fresh
+// counters count the positions whose codes differ, and a word is a candidate
+// iff at most k positions differ: exactly hamming_bounded's test
+// (edit_distance.hpp:18-27), so the verifier sees only true matches.
+template <int NP, int FW, int EXTRA, int S, bool HOT, bool X = false>
 __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __restrict__ tiles, uint32_t ntiles,
                                                             const __grid_constant__ SliceParams P) {
     using Sh = SliceShape<NP, FW, EXTRA, S>;
@@ -449,6 +456,15 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                     }
                     return x;
                 }
+                if constexpr (X) {
+                    if (i >= NF + EXTRA) {  // byte position p: its kXBits code planes differ anywhere
+                        const int b0 = NP + kXBits * (i - NF - EXTRA);
+                        uint32_t x = qxor(pl[r][b0], FPG_QS(h, b0), FPG_QM(h, b0));
+#pragma unroll
+                        for (int u = 1; u < kXBits; ++u) x |= qxor(pl[r][b0 + u], FPG_QS(h, b0 + u), FPG_QM(h, b0 + u));
+                        return x;
+                    }
+                }
                 const int b = i < NF + EXTRA ? i - NF : NP + (i - NF - EXTRA);
                 return qxor(pl[r][b], FPG_QS(h, b), FPG_QM(h, b));
             };
@@ -517,13 +533,28 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 }
             }
             if (verify) {
-                if (!o_exhaustive)
+                if constexpr (X) {
+                    static_assert(S == kXBits * kXLen, "exact path planes");
+#pragma unroll
+                    for (int h = 0; h < NQ; ++h)
+#pragma unroll
+                        for (int r = 0; r < SLX; ++r) {
+                            co[h][r] = ct[h][r] = 0u;
+                            cf[h][r] = ~valid[r];
+                        }
+                    count(std::integral_constant<int, NF + EXTRA>{}, std::integral_constant<int, NF + EXTRA + kXLen>{});
+                } else if (!o_exhaustive) {
                     count(std::integral_constant<int, NF + EXTRA>{}, std::integral_constant<int, NF + EXTRA + S>{});
+                }
+                // exact path: at most k differing positions, ~(f | t) at k = 1
+                auto exact_pass = [&](int h, int r) -> uint32_t {
+                    return o_k ? lop3<0x03>(cf[h][r], ct[h][r], 0u) : lop3<0x01>(cf[h][r], ct[h][r], co[h][r]);
+                };
 #pragma unroll
                 for (int h = 0; h < NQ; ++h)
 #pragma unroll
                     for (int r = 0; r < SLX; ++r) {
-                        const uint32_t cand = o_exhaustive ? valid[r] : passed(h, r);
+                        const uint32_t cand = X ? exact_pass(h, r) : o_exhaustive ? valid[r] : passed(h, r);
                         if (cand) {
                             s_queue[qn * kSliceThreads + tid] = make_uint2(jq[h] | ((row0 + (uint32_t)r) << 16), cand);
                             ++qn;

@@ -611,8 +611,11 @@ class Batch:
         cand, scan = ctypes.c_uint64(), ctypes.c_uint64()
         check(self._lib.fpg_batch_last_candidates(self._h, shard, ctypes.byref(cand)))
         check(self._lib.fpg_batch_last_scanned(self._h, shard, ctypes.byref(scan)))
+        scan_x = ctypes.c_uint64()
+        check(self._lib.fpg_batch_last_scanned_exact(self._h, shard, ctypes.byref(scan_x)))
         return {"run_ms": run_ms.value, "filter_ms": filt_ms.value, "executed_pairs": ex.value,
-                "survivors": sv.value, "launches": ln.value, "candidates": cand.value, "scanned_pairs": scan.value}
+                "survivors": sv.value, "launches": ln.value, "candidates": cand.value, "scanned_pairs": scan.value,
+                "scanned_pairs_exact": scan_x.value}
 
     def host_ms(self) -> dict:
         """Host-side ms of the last upload, download (D2H wait) and result
