@@ -852,6 +852,18 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
             if (!pl.empty())
                 CK(cudaMemcpyAsync(dev.p, pl.data(), pl.size() * sizeof(fpg::SliceTile), cudaMemcpyHostToDevice, st));
         };
+        // a small exact share does not pay for its own launch (latency-bound
+        // batches): those tiles go back to the sig' path
+        // (FPG_EXACT_MIN: pair threshold, read per plan so tests can force the path)
+        uint64_t x_pairs = 0;
+        for (const auto& t : splan_x) x_pairs += (uint64_t)t.q_count * t.n_slabs * 32u;
+        if ((double)x_pairs < env_double("FPG_EXACT_MIN", 67108864.0)) {
+            for (auto t : splan_x) {
+                t.plane_base = W.plane_base[t.w_len];
+                splan.push_back(t);
+            }
+            splan_x.clear();
+        }
         finish_plan(splan, S.stiles);
         finish_plan(splan_x, S.stiles_x);
     } else {

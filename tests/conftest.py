@@ -23,6 +23,18 @@ def gpu_available() -> bool:
         return False
 
 
+@pytest.fixture(params=["exact-auto", "exact-forced"])
+def exact_path(request, monkeypatch):
+    """Runs a test twice: with K2's exact short-word Hamming path at its
+    default work threshold (small test batches then stay on the sig' path),
+    and forced on for every eligible tile (FPG_EXACT_MIN=0)."""
+    if request.param == "exact-forced":
+        monkeypatch.setenv("FPG_EXACT_MIN", "0")
+    else:
+        monkeypatch.delenv("FPG_EXACT_MIN", raising=False)
+    return request.param
+
+
 @pytest.fixture(scope="session")
 def oracle():
     from oracle.oracle import Oracle

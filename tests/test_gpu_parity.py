@@ -91,7 +91,7 @@ def _fixture_case(q):
 
 
 @pytest.mark.parametrize("case", range(len(GOLD["queries"])))
-def test_queries_match_reference_fixture(case):
+def test_queries_match_reference_fixture(case, exact_path):
     q = GOLD["queries"][case]
     s = fixture_scheme(_fixture_case(q))
     words = [bytes.fromhex(h) for h in GOLD["query_dict"]]
@@ -136,7 +136,7 @@ def _cfg_inputs(cfg, n, nq):
 
 @pytest.mark.parametrize("cfg,n,nq", [(1, 100_000, 1000), (2, 200_000, 600), (3, 200_000, 600), (4, 50_000, 300),
                                       (5, 200_000, 600)])
-def test_config_cells_vs_oracle(oracle, cfg, n, nq):
+def test_config_cells_vs_oracle(oracle, cfg, n, nq, exact_path):
     blob, offs, qblob, qoffs = _cfg_inputs(cfg, n, nq)
     for variant, width, b, p, metric in CELLS[cfg]:
         s = make_scheme(blob, variant, width, b, p)
@@ -151,7 +151,7 @@ def test_config_cells_vs_oracle(oracle, cfg, n, nq):
 
 @pytest.mark.parametrize("metric", [Metric.Hamming, Metric.Levenshtein])
 @pytest.mark.parametrize("k", [0, 1, 2, 3])
-def test_filter_off_and_k0(oracle, metric, k):
+def test_filter_off_and_k0(oracle, metric, k, exact_path):
     """k = 0..3 (k >= 2 runs the generic kernel and the banded verifier), filter on/off."""
     blob, offs, qblob, qoffs = _cfg_inputs(2, 50_000, 300)
     s = make_scheme(blob, Variant.Count, 16)
@@ -165,7 +165,7 @@ def test_filter_off_and_k0(oracle, metric, k):
     assert np.array_equal(csr.offsets, naive_off) and np.array_equal(csr.word_ids, naive_ids)
 
 
-def test_edge_strings(oracle):
+def test_edge_strings(oracle, exact_path):
     """Empty strings, 1-byte strings, zero bytes, 0xff, duplicates, long strings."""
     rng = np.random.default_rng(7)
     words = [b"", b"", b"a", b"\x00", b"a\x00", b"\x00a", b"\xff" * 3, b"ab", b"ba"]
@@ -242,7 +242,7 @@ def test_too_long_and_invalid_args():
         assert len(csr) == 0 and st.shape == (0, 5)
 
 
-def test_shards_equal_single_device(oracle):
+def test_shards_equal_single_device(oracle, exact_path):
     """Dictionary sharded over [0,0,0] (three shards on one GPU, independent
     kernels) gives the single-shard answer with rebased ids."""
     blob, offs, qblob, qoffs = _cfg_inputs(5, 100_000, 400)
@@ -270,7 +270,7 @@ def test_output_regrowth_many_matches(oracle):
     assert_same(csr, st, *oracle.query_batch(blob, offs, qblob, qoffs, osch(s), Metric.Levenshtein, 1, True, True))
 
 
-def test_k4_segment_size_classes(oracle):
+def test_k4_segment_size_classes(oracle, exact_path):
     """K4 sorts each query's matches by word id in one of three ways: <= 32
     (warp bitonic), 33..4096 (one CTA, shared-memory bitonic) and larger
     (value-range buckets, per-warp sorts), with a CUB fallback when one bucket
@@ -298,7 +298,7 @@ def test_k4_segment_size_classes(oracle):
         assert_same(csr, st, *oracle.query_batch(blob, offs, qblob, qoffs, osch(s), metric, 1, True, True))
 
 
-def test_staged_batch_reruns_across_options(oracle):
+def test_staged_batch_reruns_across_options(oracle, exact_path):
     """One upload, several runs (fpg_batch_run) with options whose outputs
     differ in size and shape: the cached tile plan and the K4 path choice
     (segmented vs radix sort, chosen per batch) must follow the options."""
