@@ -68,7 +68,10 @@ def alu_peak():
         return 64.0, "unmeasured: 16 lanes/clk/SMSP (B300_MICROARCH.md pipe rates)"
 
 
-def ops_per_comparison(scheme, sig_fields: int) -> float:
+X_LEN, X_BITS = 4, 5  # the exact Hamming path of short words (fpg_kernels.cuh kXLen / kXBits)
+
+
+def ops_per_comparison(scheme, sig_fields: int, exact: bool = False) -> float:
     """LOP3 per comparison of the bit-sliced test (fpg_slice.cuh): per 32-word
     slab, the ORs folding a multi-bit field's planes (1 for 2-3 bits, 2 for 4
     bits), then the carry-save counter: 6 per four field bits plus one
@@ -90,6 +93,8 @@ def ops_per_comparison(scheme, sig_fields: int) -> float:
         return 6 * q4 + (q4 + 1) // 2 + 4 * ((n % 4 + 1) // 2)
 
     ors = nf * (0 if fw == 1 else 1 if fw <= 3 else 2)
+    if exact:  # position fields: a 5-plane OR (2 LOP3) each, then their own counter
+        return (ors + csa(nf + extra) + 2 * X_LEN + csa(X_LEN) + 1) / 32.0
     return (ors + csa(nf + extra) + csa(sig_fields) + 1) / 32.0
 
 
@@ -504,13 +509,19 @@ def main():
     filt_avg_ms = statistics.mean(f[0] for f in filt_ms)
     achieved = t0s["scanned_pairs"] / (filt_avg_ms / 1e3) / 1e12
     shape = d.scan_shape()
-    ops = ops_per_comparison(w.scheme, shape["sig_fields"])
+    # LOP3 per comparison, weighted over the sig' launch and the exact path's
+    pairs_x = t0s.get("scanned_pairs_exact", 0)
+    pairs_m = t0s["scanned_pairs"] - pairs_x
+    ops = ((pairs_m * ops_per_comparison(w.scheme, shape["sig_fields"]) +
+            pairs_x * ops_per_comparison(w.scheme, shape["sig_fields"], exact=True)) /
+           max(pairs_m + pairs_x, 1))
     lop3_clk, lop3_basis = alu_peak()
     popc_peak = sms * sm_mhz * 1e6 * POPC_PER_CLK_PER_SM / math.ceil(w.scheme.width() / 32) / 1e12
     if shape["sliced"]:
         peak = sms * sm_mhz * 1e6 * lop3_clk / ops / 1e12
         bound, basis = "int-alu", (f"{sms} SMs x {sm_mhz:.0f} MHz x {lop3_clk:.1f} LOP3/clk/SM ({lop3_basis}) / "
-                                   f"{ops:.3f} LOP3 per comparison (bit-sliced test, {shape['sig_fields']} sig' planes)")
+                                   f"{ops:.3f} LOP3 per comparison (bit-sliced test, {shape['sig_fields']} sig' planes; "
+                                   f"exact-path pairs weighted with their own count)")
     else:
         peak = popc_peak
         bound, basis = "int-xu", f"{sms} SMs x {sm_mhz:.0f} MHz x {POPC_PER_CLK_PER_SM} POPC/clk/SM / ceil(W/32)"
@@ -524,6 +535,7 @@ def main():
         "queries_per_s": w.nq * args.steps / (total_ms / 1e3),
         "executed_pairs_per_step": sum(t["executed_pairs"] for t in t_last),
         "evaluated_pairs_per_step": sum(t["scanned_pairs"] for t in t_last),
+        "exact_path_pairs_per_step": sum(t.get("scanned_pairs_exact", 0) for t in t_last),
         "survivors_per_step": sum(t["survivors"] for t in t_last),
         "verifier_candidates_per_step": sum(t["candidates"] for t in t_last),
         "matches_per_step": int(csr.offsets[-1]) if world == 1 else None,

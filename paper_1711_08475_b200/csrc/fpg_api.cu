@@ -231,7 +231,7 @@ struct Collection {
     std::vector<uint64_t> xplane_base;  // per length <= kXLen: u32 offset in xplanes
     DBuf<uint64_t> d_xplane_base;
     DBuf<uint2> slab_w;       // bit-sliced dictionary: group-weight box (min, max bytes) per global slab
-    DBuf<uint32_t> wkey_a, wkey_b;  // scratch: (length << 16 | group weights) sort keys
+    DBuf<uint64_t> wkey_a, wkey_b;  // scratch: (length << 32 | group weights) sort keys
     DBuf<uint32_t> d_slab_start, d_count;
     DBuf<uint64_t> d_plane_base;
     // scratch (len_b = lengths in sorted order; kept for query collections)
@@ -352,14 +352,14 @@ struct Collection {
             if (prof) {
                 stage_mark(st);
                 // offsets and word bytes in, (length, group weights) keys out
-                stage_add("k_weight_keys", 8.0 * (n + 1) + (double)blob_bytes + 4.0 * n);
+                stage_add("k_weight_keys", 8.0 * (n + 1) + (double)blob_bytes + 8.0 * n);
             }
             CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, wkey_a.p, wkey_b.p, idx_a.p, idx_b.p, (int)n, 0,
-                                               end_bit + 16, st));
+                                               end_bit + 32, st));
             cub_tmp.reserve(tmp);
             if (prof) stage_mark(st);
             CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, tmp, wkey_a.p, wkey_b.p, idx_a.p, idx_b.p, (int)n, 0,
-                                               end_bit + 16, st));
+                                               end_bit + 32, st));
             wt.reserve(n);
         } else {
             CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, len_a.p, len_b.p, idx_a.p, idx_b.p, (int)n, 0,
@@ -372,8 +372,8 @@ struct Collection {
         if (prof) {
             stage_mark(st);
             // CUB onesweep (library): one read + write of keys and values per 8-bit digit pass
-            const int passes = ((mode == kSliceDict ? end_bit + 16 : end_bit) + 7) / 8;
-            stage_add("cub_radix_sort", passes * 2.0 * (mode == kSliceDict ? 8.0 : 6.0) * n);
+            const int passes = ((mode == kSliceDict ? end_bit + 32 : end_bit) + 7) / 8;
+            stage_add("cub_radix_sort", passes * 2.0 * (mode == kSliceDict ? 12.0 : 6.0) * n);
         }
         uint64_t* cmp_p = mode == kGenericDict ? cmp.p : nullptr;
         uint32_t* sig_p = mode == kGenericDict ? sig.p : nullptr;

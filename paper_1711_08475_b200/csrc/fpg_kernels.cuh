@@ -150,21 +150,22 @@ __device__ __forceinline__ uint64_t onehot_count16(uint64_t fp) {
     return r;
 }
 
-// Group weights: the fields are dealt round robin into 4 groups (field i ->
-// group i & 3; occurrence / halved: bit i, count / position: the extra
-// one-bit fields, then the multi-bit fields), and byte g of the result is the
-// number of "present" fields of group g (occurrence / halved: set bits;
-// count: non-zero counters; position: letters whose first position is
-// recorded, plus the extra occurrence bits).  One differing field changes one
-// group's weight by at most one, so
+// Group weights: the fields are dealt round robin into kGroups = 8 groups
+// (field i -> group i & 7; occurrence / halved: bit i, count / position: the
+// extra one-bit fields, then the multi-bit fields), and nibble g of the
+// result is the number of "present" fields of group g (occurrence / halved:
+// set bits; count: non-zero counters; position: letters whose first position
+// is recorded, plus the extra occurrence bits; at most 8 per group for
+// W <= 64).  One differing field changes one group's weight by at most one, so
 //   sum_g |gw_g(a) - gw_g(b)| <= F_D          (fingerprint.hpp:171-214)
 // and K2 skips query / word groups whose group-weight boxes are more than 2k
 // apart (L1 distance).
+constexpr int kGroups = 8;
 __device__ __forceinline__ uint32_t fp_gweight(uint64_t fp, const SchemeParams& P) {
     if (P.variant == 0 || P.variant == 1) {
         uint32_t w = 0;
 #pragma unroll
-        for (int g = 0; g < 4; ++g) w |= (uint32_t)__popcll(fp & (0x1111111111111111ull << g)) << (8 * g);
+        for (int g = 0; g < kGroups; ++g) w |= (uint32_t)__popcll(fp & (0x0101010101010101ull << g)) << (4 * g);
         return w;
     }
     const int fw = P.variant == 2 ? P.b : P.p;
@@ -172,24 +173,23 @@ __device__ __forceinline__ uint32_t fp_gweight(uint64_t fp, const SchemeParams& 
     const int extra = P.variant == 2 ? 0 : P.extra;
     const uint64_t fmask = fw >= 64 ? ~0ull : ((1ull << fw) - 1);
     uint32_t w = 0;
-    for (int e = 0; e < extra; ++e) w += (uint32_t)((fp >> e) & 1u) << (8 * (e & 3));
+    for (int e = 0; e < extra; ++e) w += (uint32_t)((fp >> e) & 1u) << (4 * (e & 7));
     for (int f = 0; f < nf; ++f) {
         const uint64_t v = (fp >> (P.width - fw * (f + 1))) & fmask;
         const bool present = P.variant == 2 ? (v != 0) : (v != fmask);  // position: all-ones = absent
-        w += (uint32_t)present << (8 * ((extra + f) & 3));
+        w += (uint32_t)present << (4 * ((extra + f) & 7));
     }
     return w;
 }
 
-// Sort keys of the dictionary's K2 layout: (length << 16 | group weights, 4
-// bits each, saturated at 15, group 0 most significant) per word in input
-// order (the fingerprint is computed here and again by k_build).  Saturation
-// only coarsens the order; K2's ranges use the exact group weights.
+// Sort keys of the dictionary's K2 layout: length << 32 | the group weights
+// with group 0 in the most significant nibble, per word in input order (the
+// fingerprint is computed here and again by k_build).
 template <int VARIANT>
 __global__ void __launch_bounds__(256) k_weight_keys(const uint8_t* __restrict__ blob,
                                                      const uint64_t* __restrict__ offsets, uint64_t n,
                                                      const __grid_constant__ SchemeParams P,
-                                                     uint32_t* __restrict__ keys) {
+                                                     uint64_t* __restrict__ keys) {
     __shared__ int8_t s_slot[256];
     s_slot[threadIdx.x] = P.slot[threadIdx.x];
     __syncthreads();
@@ -214,8 +214,8 @@ __global__ void __launch_bounds__(256) k_weight_keys(const uint8_t* __restrict__
     const uint32_t gw = fp_gweight(fb.bits, P);
     uint32_t key = 0;
 #pragma unroll
-    for (int g = 0; g < 4; ++g) key |= min((gw >> (8 * g)) & 0xffu, 15u) << (12 - 4 * g);
-    keys[i] = ((uint32_t)len << 16) | key;
+    for (int g = 0; g < kGroups; ++g) key |= ((gw >> (4 * g)) & 0xfu) << (28 - 4 * g);
+    keys[i] = ((uint64_t)len << 32) | key;
 }
 
 // Inputs: raw blob + offsets, `order` = sorted position -> input index (stable

@@ -125,8 +125,8 @@ struct SliceParams {
     int32_t stats;
     int32_t use_fp;             // scheme fields bound this metric (variant_supports, fingerprint.hpp:36-38)
     int32_t wskip;              // skip query / slab-group pairs whose weights differ by more than 2k
-    const uint32_t* q_weight;   // per sorted query: group weights (fp_gweight, one byte per group)
-    const uint2* slab_w;        // per global slab: per-byte min / max of its words' group weights
+    const uint32_t* q_weight;   // per sorted query: group weights (fp_gweight, one nibble per group)
+    const uint2* slab_w;        // per global slab: per-nibble min / max of its words' group weights
     unsigned long long* scanned;  // pairs actually evaluated (after the weight skip)
     int32_t exhaustive;         // verify every pair: no fingerprint / sig' pruning (naive-path timing)
     int32_t drop_candidates;    // A/B diagnosis only (FPG_DROP_CANDIDATES=1): queued candidates are discarded unverified
@@ -145,19 +145,33 @@ __device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
     asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(LUT));
     return d;
 }
-// Per-byte min of lo and max of hi over the warp: a group-weight box.
+// Group weights are 8 nibbles (fp_gweight); the video intrinsics work on
+// bytes, so even and odd nibbles are handled as two byte vectors.
+constexpr uint32_t kNib = 0x0f0f0f0fu;
+__device__ __forceinline__ uint32_t nib_min(uint32_t a, uint32_t b) {
+    return __vminu4(a & kNib, b & kNib) | (__vminu4((a >> 4) & kNib, (b >> 4) & kNib) << 4);
+}
+__device__ __forceinline__ uint32_t nib_max(uint32_t a, uint32_t b) {
+    return __vmaxu4(a & kNib, b & kNib) | (__vmaxu4((a >> 4) & kNib, (b >> 4) & kNib) << 4);
+}
+// Per-nibble min of lo and max of hi over the warp: a group-weight box.
 __device__ __forceinline__ uint2 warp_box(uint32_t lo, uint32_t hi) {
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
-        lo = __vminu4(lo, __shfl_xor_sync(0xffffffffu, lo, d));
-        hi = __vmaxu4(hi, __shfl_xor_sync(0xffffffffu, hi, d));
+        lo = nib_min(lo, __shfl_xor_sync(0xffffffffu, lo, d));
+        hi = nib_max(hi, __shfl_xor_sync(0xffffffffu, hi, d));
     }
     return make_uint2(lo, hi);
 }
-// L1 distance between a query's group weights and a box: at most one of the
-// two saturated differences of a byte is non-zero.
-__device__ __forceinline__ uint32_t box_dist(uint32_t q, uint2 box) {
-    return __vsadu4(__vsubus4(box.x, q) | __vsubus4(q, box.y), 0u);
+// A box split into even / odd nibble byte vectors: (lo even, lo odd, hi even, hi odd).
+__device__ __forceinline__ uint4 split_box(uint2 box) {
+    return make_uint4(box.x & kNib, (box.x >> 4) & kNib, box.y & kNib, (box.y >> 4) & kNib);
+}
+// L1 distance between a query's group weights (split: even, odd nibbles) and
+// a split box: at most one of the two saturated differences of a group is
+// non-zero.
+__device__ __forceinline__ uint32_t box_dist(uint32_t qe, uint32_t qo, uint4 b) {
+    return __vsadu4(__vsubus4(b.x, qe) | __vsubus4(qe, b.z), 0u) + __vsadu4(__vsubus4(b.y, qo) | __vsubus4(qo, b.w), 0u);
 }
 
 template <int NP, int FW, int EXTRA, int S>
@@ -207,7 +221,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
     __shared__ uint32_t s_grp;  // next slab group of the tile
     __shared__ uint32_t s_next[2];  // next tile index, double-buffered by iteration parity
     __shared__ uint32_t s_surv[kSliceQ];
-    __shared__ uint32_t s_qw[kSliceQ];  // query group weights
+    __shared__ uint32_t s_qw[2][kSliceQ];  // query group weights: even, odd nibbles (byte vectors)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     unsigned long long surv_warp = 0;  // lanes 0, 1: the warp's fingerprint survivors
     uint32_t cand_lane = 0;
@@ -243,7 +257,9 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
             s_qinfo[j] = (uint32_t)m;
             s_qid[j] = id;
             s_surv[j] = 0u;
-            s_qw[j] = o_wskip ? P.q_weight[qp] : 0u;
+            const uint32_t qw = o_wskip ? P.q_weight[qp] : 0u;
+            s_qw[0][j] = qw & kNib;
+            s_qw[1][j] = (qw >> 4) & kNib;
         }
         // this lane's slabs of slab group g (SL rows of 32 slabs), the
         // group's valid words and its group-weight box
@@ -275,8 +291,8 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 vw += __popc(valid[r]);
                 if (ok && o_wskip) {
                     const uint2 mm = __ldg(P.slab_w + tl.slab_g0 + slab);
-                    wlo = __vminu4(wlo, mm.x);
-                    whi = __vmaxu4(whi, mm.y);
+                    wlo = nib_min(wlo, mm.x);
+                    whi = nib_max(whi, mm.y);
                 }
             }
             box = make_uint2(wlo, whi);
@@ -586,11 +602,12 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 if (g >= n_grp) break;
                 row0 = (uint32_t)SL * g;
                 box = warp_box(box.x, box.y);
+                const uint4 sbox = split_box(box);
                 uint32_t nlist = 0;
                 for (uint32_t b = 0; b < tl.q_count; b += 32) {
                     const uint32_t j = b + (uint32_t)lane;
                     bool in = j < tl.q_count;
-                    if (in && o_wskip) in = box_dist(s_qw[j], box) <= span;
+                    if (in && o_wskip) in = box_dist(s_qw[0][j], s_qw[1][j], sbox) <= span;
                     const uint32_t bal = __ballot_sync(0xffffffffu, in);
                     if (in) ql[nlist + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)j;
                     nlist += __popc(bal);
@@ -671,7 +688,7 @@ __global__ void __launch_bounds__(32 * kPlanesSlabs) k_planes(
         const bool ok = wi < count[L];
         const uint64_t f = ok ? fp[start[L] + wi] : 0ull;
         const uint32_t g = ok ? sigp[start[L] + wi] : 0u;
-        if (slab_w) {  // the slab's group-weight box (K2's weight window): per-byte min / max
+        if (slab_w) {  // the slab's group-weight box (K2's weight window): per-nibble min / max
             const uint32_t wt = ok ? weight[start[L] + wi] : 0u;
             const uint2 box = warp_box(ok ? wt : 0xffffffffu, ok ? wt : 0u);
             if (lane == 0) slab_w[gs] = box;

@@ -20,22 +20,25 @@ CELLS = [(0, 16, 2, 3), (0, 32, 2, 3), (0, 64, 2, 3), (1, 16, 2, 3), (1, 32, 2, 
          (2, 16, 2, 3), (2, 32, 2, 3), (2, 64, 4, 3), (3, 16, 2, 3), (3, 32, 2, 3), (3, 64, 2, 3)]
 
 
+GROUPS = 8  # kGroups in fpg_kernels.cuh
+
+
 def fp_gweight(fp: int, variant: int, width: int, b: int, p: int) -> list[int]:
-    """Per-group count of "present" fields; field i goes to group i & 3."""
-    g = [0, 0, 0, 0]
+    """Per-group count of "present" fields; field i goes to group i & 7."""
+    g = [0] * GROUPS
     if variant in (0, 1):
         for i in range(width):
-            g[i & 3] += (fp >> i) & 1
+            g[i % GROUPS] += (fp >> i) & 1
         return g
     fw = b if variant == 2 else p
     nf = width // fw
     extra = 0 if variant == 2 else width - fw * nf
     fmask = (1 << fw) - 1
     for e in range(extra):
-        g[e & 3] += (fp >> e) & 1
+        g[e % GROUPS] += (fp >> e) & 1
     for f in range(nf):
         v = (fp >> (width - fw * (f + 1))) & fmask
-        g[(extra + f) & 3] += int(v != 0) if variant == 2 else int(v != fmask)
+        g[(extra + f) % GROUPS] += int(v != 0) if variant == 2 else int(v != fmask)
     return g
 
 
@@ -83,10 +86,11 @@ def test_group_weight_distance_bounds_fd(oracle, variant, width, b, p):
     assert tight > 0  # the bound is reached, i.e. it is not vacuous
 
 
-def test_group_weights_fit_the_sort_key():
-    """k_weight_keys packs the group weights saturated at 15 below the length;
-    saturation is 1-Lipschitz, so it can only coarsen the order."""
-    rng = np.random.default_rng(0)
-    a = rng.integers(0, 40, size=1000)
-    b = rng.integers(0, 40, size=1000)
-    assert np.all(np.abs(np.minimum(a, 15) - np.minimum(b, 15)) <= np.abs(a - b))
+@pytest.mark.parametrize("variant,width,b,p", CELLS)
+def test_group_weights_fit_a_nibble(oracle, variant, width, b, p):
+    """Group weights travel as 8 nibbles (sort key, slab boxes, K2's window):
+    no group can hold more than 15 present fields at W <= 64."""
+    cap = oracle.letter_capacity(variant, width, b, p)
+    sch = oscheme(variant, ALPHABET[:cap], width, b, p)
+    fp = (1 << width) - 1 if variant != 3 else 0  # every field present (position: all-zero fields)
+    assert max(fp_gweight(fp, variant, width, b, p)) <= 15
