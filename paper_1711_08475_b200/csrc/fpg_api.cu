@@ -230,7 +230,10 @@ struct Collection {
     DBuf<uint32_t> xplanes;   // exact path planes of the buckets L <= kXLen: fingerprint bits, then codes
     std::vector<uint64_t> xplane_base;  // per length <= kXLen: u32 offset in xplanes
     DBuf<uint64_t> d_xplane_base;
-    DBuf<uint2> slab_w;       // bit-sliced dictionary: group-weight box (min, max bytes) per global slab
+    DBuf<uint2> slab_w;       // bit-sliced dictionary: group-weight box (min, max nibbles) per global slab
+    DBuf<uint2> gbox;         // ... and per slab group (32 * SL slabs of a bucket)
+    std::vector<uint32_t> group_start;  // L1 + 1: first global slab group of each bucket
+    DBuf<uint32_t> d_group_start;
     DBuf<uint64_t> wkey_a, wkey_b;  // scratch: (length << 32 | group weights) sort keys
     DBuf<uint32_t> d_slab_start, d_count;
     DBuf<uint64_t> d_plane_base;
@@ -435,6 +438,24 @@ struct Collection {
                 stage_mark(st);
                 // fingerprints, codes, weights in; planes and slab boxes out
                 stage_add("k_planes", 16.0 * n + 4.0 * (double)pb + 8.0 * (double)sl);
+            }
+            // group boxes: the unit K2 warps claim is 32 * SL slabs
+            const uint32_t gsl = (uint32_t)fpg::slice_group_slabs(npt);
+            group_start.assign(L1 + 1, 0);
+            uint32_t ng = 0;
+            for (int L = 0; L < L1; ++L) {
+                group_start[L] = ng;
+                ng += (uint32_t)cdiv(count[L] ? cdiv(count[L], 32) : 0, gsl);
+            }
+            group_start[L1] = ng;
+            gbox.reserve(std::max<uint32_t>(ng, 1));
+            d_group_start.reserve(L1 + 1);
+            CK(cudaMemcpyAsync(d_group_start.p, group_start.data(), sizeof(uint32_t) * (L1 + 1), cudaMemcpyHostToDevice, st));
+            if (ng) {
+                fpg::k_group_box<<<(unsigned)cdiv(ng, 256), 256, 0, st>>>(slab_w.p, d_slab_start.p, d_group_start.p, L1,
+                                                                          ng, gsl, gbox.p);
+                CK(cudaGetLastError());
+                ++launches;
             }
             if (P.xlen) {
                 // exact path planes (same kernel): fingerprint bits, then the
@@ -798,6 +819,7 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
                     t.w_stride = (uint16_t)stride_of(lw);
                     t.count_only = count_only ? 1u : 0u;
                     t.slab_g0 = W.slab_start[lw];
+                    t.gbox_base = W.group_start[lw] + s0 / grp;
                     const bool xt = xpath && lw <= fpg::kXLen && !count_only;
                     if (xt) t.plane_base = W.xplane_base[lw];
                     (xt ? splan_x : splan).push_back(t);
@@ -931,6 +953,7 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         SP.wskip = SP.use_fp && !o.exhaustive && !g_no_wskip ? 1 : 0;
         SP.q_weight = Q.wt.p;
         SP.slab_w = W.slab_w.p;
+        SP.gbox = W.gbox.p;
         SP.scanned = S.counters.p + 6;
         static const int drop = (int)env_double("FPG_DROP_CANDIDATES", 0.0);
         SP.drop_candidates = drop;

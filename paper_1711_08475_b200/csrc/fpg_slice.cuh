@@ -98,6 +98,8 @@ struct SliceTile {
     uint16_t w_len, w_stride;
     uint32_t count_only;   // fingerprint survivors counted, never verified
     uint32_t slab_g0;      // global index of the bucket's first slab (slab_w)
+    uint32_t gbox_base;    // index in gbox of the tile's first slab group
+    uint32_t pad_;
 };
 
 struct SliceParams {
@@ -127,6 +129,7 @@ struct SliceParams {
     int32_t wskip;              // skip query / slab-group pairs whose weights differ by more than 2k
     const uint32_t* q_weight;   // per sorted query: group weights (fp_gweight, one nibble per group)
     const uint2* slab_w;        // per global slab: per-nibble min / max of its words' group weights
+    const uint2* gbox;          // per slab group of a bucket (32 * SL slabs): the union of its slabs' boxes
     unsigned long long* scanned;  // pairs actually evaluated (after the weight skip)
     int32_t exhaustive;         // verify every pair: no fingerprint / sig' pruning (naive-path timing)
     int32_t drop_candidates;    // A/B diagnosis only (FPG_DROP_CANDIDATES=1): queued candidates are discarded unverified
@@ -289,13 +292,9 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 const uint32_t rem = tl.w_count - 32u * slab;  // words left in the bucket from this slab on
                 valid[r] = !ok ? 0u : rem >= 32u ? 0xffffffffu : ((1u << rem) - 1u);
                 vw += __popc(valid[r]);
-                if (ok && o_wskip) {
-                    const uint2 mm = __ldg(P.slab_w + tl.slab_g0 + slab);
-                    wlo = nib_min(wlo, mm.x);
-                    whi = nib_max(whi, mm.y);
-                }
             }
-            box = make_uint2(wlo, whi);
+            // the group's weight box, precomputed at construction (k_group_box)
+            box = o_wskip ? __ldg(P.gbox + tl.gbox_base + g) : make_uint2(wlo, whi);
         };
         // warp w's first group is group w: its planes load while the queries
         // are set up; later groups are claimed from s_grp
@@ -601,7 +600,6 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 }
                 if (g >= n_grp) break;
                 row0 = (uint32_t)SL * g;
-                box = warp_box(box.x, box.y);
                 const uint4 sbox = split_box(box);
                 uint32_t nlist = 0;
                 for (uint32_t b = 0; b < tl.q_count; b += 32) {
@@ -710,6 +708,33 @@ __global__ void __launch_bounds__(32 * kPlanesSlabs) k_planes(
             planes[plane_base[L] + (uint64_t)b * ns + (g - slab_start[L])] = tile[b][lane];
         }
     }
+}
+#endif
+
+// Weight box of every slab group (gsl consecutive slabs of a bucket, the unit
+// a K2 warp claims): per-nibble min / max over its slabs' boxes.  One thread
+// per group.
+#ifndef FPG_K2_TU  // defined once, in fpg_api.cu
+__global__ void k_group_box(const uint2* __restrict__ slab_w, const uint32_t* __restrict__ slab_start,
+                            const uint32_t* __restrict__ group_start, int nlen, uint32_t total_groups, uint32_t gsl,
+                            uint2* __restrict__ gbox) {
+    const uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gi >= total_groups) return;
+    int lo = 0, hi = nlen;  // bucket: largest L with group_start[L] <= gi
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (group_start[mid] <= gi) lo = mid;
+        else hi = mid;
+    }
+    const uint32_t ns = slab_start[lo + 1] - slab_start[lo];
+    const uint32_t s0 = (gi - group_start[lo]) * gsl;
+    uint32_t wlo = 0xffffffffu, whi = 0u;
+    for (uint32_t s = s0; s < s0 + gsl && s < ns; ++s) {
+        const uint2 mm = slab_w[slab_start[lo] + s];
+        wlo = nib_min(wlo, mm.x);
+        whi = nib_max(whi, mm.y);
+    }
+    gbox[gi] = make_uint2(wlo, whi);
 }
 #endif
 

@@ -3,7 +3,7 @@
 # usage: bash tools/ncu_cell.sh <tag> <cfg> <cell> [extra env]
 tag=$1; cfg=$2; cell=$3; shift 3
 o=gpurun_out/$tag; mkdir -p $o
-env "$@" timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_slice -s 1 -c 1 -o $o/k_slice \
+env "$@" timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:${KREGEX:-k_slice}" -s 1 -c 1 -o $o/k_slice \
     python bench.py --config $cfg --cell $cell --no-cpu-baseline --no-e2e --steps 1 --warmup 1 > $o/ncu_f.log 2>&1
 echo ncu_rc=$?
 python tools/ncu_summary.py report $o/k_slice.ncu-rep 40 > $o/k_slice_summary.txt 2>&1
