@@ -57,6 +57,10 @@ void dispatch_slice_16(int fw, int nsig, const fpg::SliceTile* tiles, uint32_t n
 void dispatch_slice_16x(int fw, const fpg::SliceTile* tiles, uint32_t ntiles, const fpg::SliceParams& P,
                         cudaStream_t st, int device) {
     constexpr int SX = fpg::kXBits * fpg::kXLen;
+    // the exact kernel claims the same slab groups as the sig' kernel (W = 16:
+    // NPT <= 32, two slabs per lane): the precomputed group boxes serve both
+    static_assert(fpg::slice_slabs_per_lane(16 + SX) == 2 && fpg::slice_slabs_per_lane(16 + 16) == 2,
+                  "exact path and sig' path must share the slab-group size");
     switch (fw) {
         case 1: launch_slice<16, 1, 0, SX, true>(tiles, ntiles, P, st, device); break;
         case 2: launch_slice<16, 2, 0, SX, true>(tiles, ntiles, P, st, device); break;
