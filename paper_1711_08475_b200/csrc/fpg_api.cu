@@ -22,6 +22,8 @@
 #include <string>
 #include <thread>
 #include <type_traits>
+#include <unordered_map>
+#include <map>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -121,6 +123,59 @@ struct HBuf {
     HBuf(const HBuf&) = delete;
     HBuf& operator=(const HBuf&) = delete;
 };
+
+// Page-locked blocks for result arrays (fpg_result): a download writes the
+// CSR straight into them (one D2H, no staging copy, no first-touch page
+// faults), and fpg_result_free returns them here for the next result of a
+// similar size.  Process-wide; idle blocks are capped at kPinnedIdleMax.
+struct PinnedPool {
+    static constexpr size_t kPinnedIdleMax = size_t(4) << 30;
+    std::mutex mu;
+    std::unordered_map<void*, size_t> owned;  // every block of the pool -> bytes
+    std::multimap<size_t, void*> idle;
+    size_t idle_bytes = 0;
+    void* get(size_t bytes) {
+        bytes = std::max<size_t>(bytes, 64);
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            auto it = idle.lower_bound(bytes);
+            if (it != idle.end() && it->first <= 2 * bytes + (size_t(1) << 20)) {
+                void* p = it->second;
+                idle_bytes -= it->first;
+                idle.erase(it);
+                return p;
+            }
+        }
+        void* p = nullptr;
+        if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess || !p) {
+            cudaGetLastError();
+            throw std::bad_alloc();
+        }
+        std::lock_guard<std::mutex> lk(mu);
+        owned[p] = bytes;
+        return p;
+    }
+    // false: not a pool block (the caller frees it)
+    bool put(void* p) {
+        if (!p) return true;
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = owned.find(p);
+        if (it == owned.end()) return false;
+        const size_t bytes = it->second;
+        if (idle_bytes + bytes > kPinnedIdleMax) {
+            owned.erase(it);
+            cudaFreeHost(p);
+        } else {
+            idle.emplace(bytes, p);
+            idle_bytes += bytes;
+        }
+        return true;
+    }
+};
+PinnedPool& pinned_pool() {
+    static PinnedPool* pool = new PinnedPool;  // never destroyed: results may outlive static teardown
+    return *pool;
+}
 
 fpg::SchemeParams make_params(const fpg_scheme& s) {
     fpg::SchemeParams P;
@@ -1240,25 +1295,33 @@ void download(fpg_batch* B, fpg_result* out) {
     const fpg_query_options& o = B->opt;
     const bool stats = o.want_stats != 0;
     const auto t0 = std::chrono::steady_clock::now();
-    for_each_shard(B->sb.size(), [&](size_t i) { download_shard(B, *B->sb[i], stats); });
-    const auto t1 = std::chrono::steady_clock::now();
-    B->download_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
     const uint64_t nq = B->nq;
     std::memset(out, 0, sizeof(*out));
     out->nq = nq;
     uint64_t total = 0;
     for (auto& s : B->sb) total += s->total;
     out->total = total;
-    out->offsets = static_cast<uint64_t*>(std::malloc(sizeof(uint64_t) * (nq + 1)));
-    out->word_ids = static_cast<uint32_t*>(std::malloc(sizeof(uint32_t) * std::max<uint64_t>(total, 1)));
-    if (!out->offsets || !out->word_ids) throw std::bad_alloc();
+    PinnedPool& pool = pinned_pool();
+    out->offsets = static_cast<uint64_t*>(pool.get(sizeof(uint64_t) * (nq + 1)));
+    out->word_ids = static_cast<uint32_t*>(pool.get(sizeof(uint32_t) * std::max<uint64_t>(total, 1)));
     if (B->sb.size() == 1) {
+        // one shard: the CSR goes straight into the result's pinned arrays
         ShardBatch& S = *B->sb[0];
-        std::memcpy(out->offsets, S.h_offsets.p, sizeof(uint64_t) * (nq + 1));
-        parallel_ranges(total, 1u << 20, [&](uint64_t lo, uint64_t hi) {
-            if (hi > lo) std::memcpy(out->word_ids + lo, S.h_ids.p + lo, sizeof(uint32_t) * (hi - lo));
-        });
+        CK(cudaSetDevice(S.sh->device));
+        cudaStream_t st = S.stream;
+        CK(cudaMemcpyAsync(out->offsets, S.offsets.p, (nq + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        if (total) CK(cudaMemcpyAsync(out->word_ids, S.ids_out, total * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        if (stats && nq) {
+            S.h_qsurv.reserve(nq);
+            CK(cudaMemcpyAsync(S.h_qsurv.p, S.qsurv.p, nq * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        }
+        CK(cudaStreamSynchronize(st));
     } else {
+        for_each_shard(B->sb.size(), [&](size_t i) { download_shard(B, *B->sb[i], stats); });
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    B->download_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    if (B->sb.size() > 1) {
         // Shards own ascending contiguous id ranges: concatenating each query's
         // shard rows in shard order yields ascending ids (oracle order).
         uint64_t pos = 0;
@@ -1279,8 +1342,7 @@ void download(fpg_batch* B, fpg_result* out) {
         });
     }
     if (stats) {
-        out->stats = static_cast<uint64_t*>(std::malloc(FPG_NSTATS * sizeof(uint64_t) * std::max<uint64_t>(nq, 1)));
-        if (!out->stats) throw std::bad_alloc();
+        out->stats = static_cast<uint64_t*>(pool.get(FPG_NSTATS * sizeof(uint64_t) * std::max<uint64_t>(nq, 1)));
         const fpg_dict* D = B->dict;
         const uint64_t N = D->n;
         // length-compatible words per query length (QueryStats bookkeeping,
@@ -1871,9 +1933,9 @@ int fpg_query_batch(fpg_dict* dict, const uint8_t* qbytes, const uint64_t* qoffs
 int fpg_result_free(fpg_result* res) {
     return guarded([&] {
         if (!res) return;
-        std::free(res->offsets);
-        std::free(res->word_ids);
-        std::free(res->stats);
+        PinnedPool& pool = pinned_pool();
+        for (void* p : {(void*)res->offsets, (void*)res->word_ids, (void*)res->stats})
+            if (!pool.put(p)) std::free(p);
         std::memset(res, 0, sizeof(*res));
     });
 }
