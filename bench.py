@@ -422,7 +422,7 @@ def main():
         batch.run(opt, want_stats=True)
     clocks = Clocks(dev0)
     clocks.start()
-    step_ms, shard_ms, filt_ms, launches = [], [], [], 0
+    step_ms, shard_ms, filt_ms, ver_ms, launches = [], [], [], [], 0
     barrier()
     clocks.open()
     for _ in range(args.steps):
@@ -434,6 +434,7 @@ def main():
         step_ms.append(max(t["run_ms"] for t in ts))  # shards run concurrently: the slowest one
         shard_ms.append([t["run_ms"] for t in ts])
         filt_ms.append([t["filter_ms"] for t in ts])
+        ver_ms.append([t.get("verify_ms", 0.0) for t in ts])
         launches += sum(t["launches"] for t in ts)
     barrier()
     clocks.close()
@@ -526,6 +527,23 @@ def main():
         peak = popc_peak
         bound, basis = "int-xu", f"{sms} SMs x {sm_mhz:.0f} MHz x {POPC_PER_CLK_PER_SM} POPC/clk/SM / ceil(W/32)"
     traffic = profiled_traffic(f"config{args.config}", w.cell_name())
+    # K3 (out-of-line byte verification, shard 0): HBM-bound.  Algorithmic
+    # bytes per launch = the 16-byte candidate records read + one padded word
+    # (its length bucket's stride) per candidate pair + an 8-byte key per match
+    ver_avg_ms = statistics.mean(v[0] for v in ver_ms)
+    hbm, hbm_basis = hbm_peak()
+    w_stride = 16 * max(1, math.ceil(w.mean_len / 16))
+    n_match0 = int(csr.offsets[-1]) if world == 1 and nsh == 1 else None
+    ver_bytes = (16.0 * t0s.get("candidate_records", 0) * t0s.get("verify_rounds", 1) + float(w_stride) * t0s["candidates"] +
+                 8.0 * (n_match0 or 0))
+    verify = None
+    if shape["sliced"] and ver_avg_ms > 0:
+        gbs = ver_bytes / (ver_avg_ms * 1e6)
+        verify = {"kernel": "k_verify (K3)", "bound": "hbm", "ms_per_step": ver_avg_ms, "algorithmic_bytes": ver_bytes,
+                  "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm, "peak_basis": hbm_basis,
+                  "candidate_records": t0s.get("candidate_records", 0), "rounds": t0s.get("verify_rounds", 1),
+                  "bytes_basis": f"16 B per record (upper bound: records of the largest round x rounds) + {w_stride} B "
+                                 "per candidate word (random 32-byte sectors in practice) + 8 B per match key"}
     line = {
         "metric": METRIC, "value": value, "unit": "comparisons/s", "n_gpus": n_gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -544,7 +562,8 @@ def main():
         "construction": construction_roofline(d),
         "gpu_launches": launches,
         "e2e": e2e,
-        "roofline": {"bound": bound, "kernel": "k_slice (K2 filter+verify)" if shape["sliced"] else "k_scan (K2)",
+        "verify": verify,
+        "roofline": {"bound": bound, "kernel": "k_slice (K2 filter)" if shape["sliced"] else "k_scan (K2)",
                      "achieved": achieved, "peak": peak, "unit": "Tcmp/s", "frac": achieved / peak,
                      "pairs_basis": "pairs K2 evaluated (length-compatible minus weight-window skips)",
                      "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",

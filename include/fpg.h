@@ -201,6 +201,13 @@ int fpg_dict_scan_shape(const fpg_dict* dict, int32_t* sliced, int32_t* sig_fiel
 /* Pairs of the last run on `shard` that reached the byte verifier (after
  * the fingerprint test and the verifier's own exact pre-filters). */
 int fpg_batch_last_candidates(const fpg_batch* batch, int32_t shard, uint64_t* candidates);
+/* K3 (out-of-line byte verification of the bit-sliced K2's candidates) in
+ * the last run on `shard`: its CUDA-event time (filter_ms of
+ * fpg_batch_last_timing excludes it), the largest number of 16-byte
+ * candidate records one K2 round wrote, and the K2 + K3 rounds the run was
+ * cut into (1 unless the records exceeded the buffer limit). */
+int fpg_batch_last_verify(const fpg_batch* batch, int32_t shard, double* verify_ms, uint64_t* records,
+                          uint32_t* rounds);
 /* Length-compatible pairs the last run on `shard` actually evaluated: the
  * executed pairs minus those skipped whole because their group weights are
  * more than 2k apart (L1 distance over 4 field groups <= F_D, so they are

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -65,8 +66,10 @@ inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 // per-run device counters: key slots reserved, survivors, tile counter, verifier
 // candidates, big segment flag, matches, pairs evaluated after the weight skip,
 // segments listed for k_seg_sort_big, its bucket overflow flag, the exact
-// path's tile counter and its pairs evaluated
-constexpr int kNumCounters = 11;
+// path's tile counter and its pairs evaluated, candidate records reserved in
+// the current K2 round, the candidate buffer's overflow flag and the largest
+// per-round record count
+constexpr int kNumCounters = 14;
 constexpr unsigned kScatterBlocks = 148 * 4;  // grid-stride K4 scatter (the count is only known on the device)
 inline int stride_of(int len) { return len <= 16 ? 16 : (len + 15) & ~15; }
 
@@ -647,8 +650,15 @@ struct ShardBatch {
     HBuf<uint32_t> h_ids, h_qsurv;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     uint64_t total = 0, executed = 0, survivors = 0, candidates = 0, scanned = 0, scanned_x = 0, launches = 0;
-    double run_ms = 0, filter_ms = 0;
+    double run_ms = 0, filter_ms = 0, verify_ms = 0;
     uint64_t out_cap = 1 << 20;
+    // K2 -> K3 candidate records (fpg_verify.cuh): capacity per round (0: sized
+    // from the plan at first use) and the K2 + K3 rounds the tile plan is cut
+    // into when one round's records would not fit
+    DBuf<uint4> cand;
+    uint64_t cand_cap = 0, cand_records = 0;
+    uint32_t cand_rounds = 1;
+    std::vector<cudaEvent_t> ev_k3;  // per round: before / after k_verify
 };
 
 }  // namespace
@@ -674,6 +684,8 @@ struct fpg_batch {
         for (auto& s : sb) {
             cudaSetDevice(s->sh->device);
             for (auto e : s->ev)
+                if (e) cudaEventDestroy(e);
+            for (auto e : s->ev_k3)
                 if (e) cudaEventDestroy(e);
             if (s->stream) cudaStreamDestroy(s->stream);
         }
@@ -818,16 +830,17 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         // Tiles = (<= kSliceMaxSlabs slabs) x (<= kSliceQ queries), largest first,
         // handed out by an atomic counter.
         const int L1 = fpg::kMaxLen + 1;
-        // Tile shape: 128 queries x 128 slab groups (the warps claim the tile's
+        // Tile shape: 128 queries x 256 slab groups (the warps claim the tile's
         // groups dynamically, so one tile's query masks serve many groups),
         // made smaller (slabs down to two groups per warp, queries down to 32,
         // slabs down to one group per warp, queries down to 16, then slabs down
         // to one group) while the batch would give fewer than ~4 tiles per
         // resident CTA.
         const uint32_t grp = (uint32_t)fpg::slice_group_slabs(D->npt);
-        // FPG_TILE_GROUPS: slab groups per full tile (A/B runs); 128 = 16 per
-        // warp, so the end-of-tile barrier waits on a smaller share of the tile
-        static const uint32_t tile_groups = (uint32_t)env_double("FPG_TILE_GROUPS", 128.0);
+        // FPG_TILE_GROUPS: slab groups per full tile (A/B runs); 256 = 32 per
+        // warp, so the end-of-tile barrier waits on a small share of the tile
+        // (config 5 K2: 64 groups 107.4 ms, 128 103.1, 256 101.4, 512 101.2)
+        static const uint32_t tile_groups = (uint32_t)env_double("FPG_TILE_GROUPS", 256.0);
         uint32_t per = tile_groups * grp, qchunk = fpg::kSliceQ;
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, sh.device);
@@ -858,8 +871,11 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         }
         auto add = [&](int lw, uint32_t qb, uint32_t qe, bool count_only) {
             const uint32_t ns = (uint32_t)cdiv(W.count[lw], 32);
-            for (uint32_t q0 = qb; q0 < qe; q0 += qchunk)
-                for (uint32_t s0 = 0; s0 < ns; s0 += per) {
+            // slab range outer, query chunks inner: the tiles running at the same
+            // time share one slab range, so its planes and the word bytes K3
+            // reads for its candidates stay in L2
+            for (uint32_t s0 = 0; s0 < ns; s0 += per)
+                for (uint32_t q0 = qb; q0 < qe; q0 += qchunk) {
                     fpg::SliceTile t{};
                     t.slab_begin = s0;
                     t.n_slabs = std::min(per, ns - s0);
@@ -982,25 +998,18 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
 
     fpg::ScanParams P{};
     fpg::SliceParams SP{};
+    fpg::VerifyParams VP{};
     if (use_slice) {
         SP.planes = W.planes.p;
         SP.q_fp = Q.fp.p;
         SP.q_sigp = Q.sigp.p;
+        SP.q_ids = Q.ids.p;
         SP.q_len = Q.len_b.p;
         SP.q_start = Q.d_start.p;
         SP.q_bbase = Q.d_byte_base.p;
-        SP.q_bytes = Q.bytes.p;
-        SP.q_ids = Q.ids.p;
-        SP.w_bytes = W.bytes.p;
-        SP.w_ids = W.ids.p;
-        SP.id_base = D->id_base + sh.base;
         SP.q_survivors = S.qsurv.p;
-        SP.out_count = S.counters.p;
         SP.survivors_total = S.counters.p + 1;
         SP.tile_counter = reinterpret_cast<unsigned int*>(S.counters.p + 2);
-        SP.candidates = S.counters.p + 3;
-        SP.q_matches = S.qsurv.p + nq;
-        SP.match_total = S.counters.p + 5;
         SP.k = o.k;
         SP.stats = (o.want_stats && o.use_filter) ? 1 : 0;
         SP.use_fp = supports(D->scheme.variant, o.metric) && !o.exhaustive ? 1 : 0;
@@ -1012,6 +1021,18 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         SP.scanned = S.counters.p + 6;
         static const int drop = (int)env_double("FPG_DROP_CANDIDATES", 0.0);
         SP.drop_candidates = drop;
+        SP.cand_count = S.counters.p + 11;
+        // K3 (k_verify): everything it needs to resolve a candidate record
+        VP.q_start = Q.d_start.p;
+        VP.q_bbase = Q.d_byte_base.p;
+        VP.q_bytes = Q.bytes.p;
+        VP.q_ids = Q.ids.p;
+        VP.w_start = W.d_start.p;
+        VP.w_bbase = W.d_byte_base.p;
+        VP.w_bytes = W.bytes.p;
+        VP.out_count = S.counters.p;
+        VP.q_matches = S.qsurv.p + nq;
+        VP.k = o.k;
     } else {
         // comparison words: the reference-layout fingerprints when the
         // collections were built for k_slice (no one-hot form, no signatures)
@@ -1048,32 +1069,104 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
     S.offsets.reserve(nq + 1);
     S.big_list.reserve(nq);
     const bool warp_sort = nq != 0;
+    // Candidate buffer of the bit-sliced path: records per K2 + K3 round.
+    // FPG_CAND_MAX_MB bounds it (default 16 GB, and a quarter of the free
+    // device memory); FPG_CAND_MAX (records) is the tests' override.
+    auto cand_limit = [&]() -> uint64_t {
+        size_t free_b = 0, total_b = 0;
+        CK(cudaMemGetInfo(&free_b, &total_b));
+        const double mb = env_double("FPG_CAND_MAX_MB", 16384.0);
+        uint64_t rec = (uint64_t)std::min<double>(mb * 1048576.0, (double)(free_b + S.cand.cap * sizeof(uint4)) / 4.0) /
+                       sizeof(uint4);
+        const double forced = env_double("FPG_CAND_MAX", 0.0);
+        if (forced > 0) rec = (uint64_t)forced;
+        return std::max<uint64_t>(rec, 1024);
+    };
+    if (use_slice && !S.cand_cap) {
+        S.cand_cap = std::min<uint64_t>(std::max<uint64_t>(executed / 64, 1u << 20), cand_limit());
+        S.cand_rounds = 1;
+    }
     for (bool first = true;; first = false) {
         S.out.reserve(S.out_cap);
         S.ids.reserve(S.out.cap);
-        P.out = SP.out = S.out.p;
-        P.out_cap = SP.out_cap = S.out.cap;
-        if (!first) {  // rescan after growing the output (K1 zeroed them the first time)
+        P.out = VP.out = S.out.p;
+        P.out_cap = VP.out_cap = S.out.cap;
+        if (!first) {  // rescan after growing a buffer (K1 zeroed them the first time)
             CK(cudaMemsetAsync(S.counters.p, 0, kNumCounters * sizeof(unsigned long long), st));
             if (nq) CK(cudaMemsetAsync(S.qsurv.p, 0, 2 * nq * sizeof(uint32_t), st));
         }
         CK(cudaEventRecord(S.ev[1], st));
-        if (use_slice && !splan.empty()) {
-            dispatch_slice(D->scheme, D->params.nsig, S.stiles.p, (uint32_t)splan.size(), SP, st, sh.device);
-            ++S.launches;
-        }
-        if (use_slice && !splan_x.empty()) {
-            // the exact path: position-code planes instead of sig', own tile
-            // counter and pair count
-            fpg::SliceParams SX = SP;
-            SX.planes = W.xplanes.p;
-            SX.q_sigp = Q.xc.p;
-            SX.tile_counter = reinterpret_cast<unsigned int*>(S.counters.p + 9);
-            SX.scanned = S.counters.p + 10;
-            fpg_host::dispatch_slice_16x(field_width_of(D->scheme), S.stiles_x.p, (uint32_t)splan_x.size(), SX, st,
-                                         sh.device);
-            ++S.launches;
-        } else if (!use_slice && !plan.empty()) {
+        if (use_slice) {
+            S.cand.reserve(S.cand_cap);
+            SP.cand = S.cand.p;
+            SP.cand_cap = S.cand_cap;
+            const uint32_t R = S.cand_rounds;
+            while (S.ev_k3.size() < 2 * (size_t)R) {
+                cudaEvent_t e = nullptr;
+                CK(cudaEventCreate(&e));
+                S.ev_k3.push_back(e);
+            }
+            // round r scans tiles [cut(pl, r), cut(pl, r + 1)) of each plan: equal shares of its work
+            auto cut = [&](const std::vector<fpg::SliceTile>& pl, uint32_t r) -> uint32_t {
+                if (r == 0) return 0;
+                if (r >= R) return (uint32_t)pl.size();
+                uint64_t work = 0, acc = 0;
+                for (const auto& t : pl) work += (uint64_t)t.q_count * t.n_slabs;
+                uint32_t i = 0;
+                for (; i < pl.size() && acc * R < work * r; ++i) acc += (uint64_t)pl[i].q_count * pl[i].n_slabs;
+                return i;
+            };
+            for (uint32_t r = 0; r < R; ++r) {
+                if (r) {  // the rounds reuse the tile counters and the record buffer
+                    CK(cudaMemsetAsync(S.counters.p + 2, 0, sizeof(unsigned long long), st));
+                    CK(cudaMemsetAsync(S.counters.p + 9, 0, sizeof(unsigned long long), st));
+                    CK(cudaMemsetAsync(S.counters.p + 11, 0, sizeof(unsigned long long), st));
+                }
+                const uint32_t a0 = cut(splan, r), a1 = cut(splan, r + 1);
+                if (a1 > a0) {
+                    dispatch_slice(D->scheme, D->params.nsig, S.stiles.p + a0, a1 - a0, SP, st, sh.device);
+                    ++S.launches;
+                }
+                const uint32_t x0 = cut(splan_x, r), x1 = cut(splan_x, r + 1);
+                if (x1 > x0) {
+                    // the exact path: position-code planes instead of sig', own tile
+                    // counter and pair count
+                    fpg::SliceParams SX = SP;
+                    SX.planes = W.xplanes.p;
+                    SX.q_sigp = Q.xc.p;
+                    SX.tile_counter = reinterpret_cast<unsigned int*>(S.counters.p + 9);
+                    SX.scanned = S.counters.p + 10;
+                    fpg_host::dispatch_slice_16x(field_width_of(D->scheme), S.stiles_x.p + x0, x1 - x0, SX, st, sh.device);
+                    ++S.launches;
+                }
+                // K3 right behind: the record count stays on the device
+                CK(cudaEventRecord(S.ev_k3[2 * r], st));
+                if (a1 > a0 || x1 > x0) {
+                    // strings of up to 16 bytes compare from four registers each, else eight
+                    // (Hamming only compares equal lengths)
+                    const bool short16 = W.max_len <= 16 && (o.metric == FPG_HAMMING || Q.max_len <= 16);
+                    auto kv = short16 ? fpg::k_verify<4> : fpg::k_verify<8>;
+                    // one resident wave: the warps in flight then work on one window of
+                    // the record stream (records of one K2 moment share a slab range), and
+                    // the buffer is swept once (FPG_VERIFY_CTAS overrides, A/B runs)
+                    static int resident[2][64] = {{0}};
+                    const int dv = sh.device & 63;
+                    if (!resident[short16][dv]) {
+                        int sms = 148, per_sm = 0;
+                        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, sh.device));
+                        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kv, fpg::kVerifyThreads, 0));
+                        resident[short16][dv] = sms * std::max(per_sm, 1);
+                    }
+                    static const unsigned forced = (unsigned)env_double("FPG_VERIFY_CTAS", 0.0);
+                    const unsigned vgrid = forced ? forced : (unsigned)resident[short16][dv];
+                    kv<<<vgrid, fpg::kVerifyThreads, 0, st>>>(VP, S.cand.p, S.counters.p + 11, S.cand_cap, S.counters.p + 5,
+                                                              S.counters.p + 3, S.counters.p + 12, S.counters.p + 13);
+                    CK(cudaGetLastError());
+                    ++S.launches;
+                }
+                CK(cudaEventRecord(S.ev_k3[2 * r + 1], st));
+            }
+        } else if (!plan.empty()) {
             dispatch_scan(D->params, D->params.onehot && !from_slice, o.want_stats != 0, S.tiles.p,
                           (uint32_t)plan.size(), P, st, sh.device);
             ++S.launches;
@@ -1104,9 +1197,25 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         }
         CK(cudaMemcpyAsync(S.h_counters.p, S.counters.p, kNumCounters * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        if (S.h_counters.p[0] <= S.out.cap) break;  // reserved key slots fit
-        S.out_cap = S.h_counters.p[0] + S.h_counters.p[0] / 4 + 1024;  // grow and rescan
+        bool redo = false;
+        if (use_slice && S.h_counters.p[12]) {
+            // a round's candidate records did not fit: a larger buffer up to the
+            // limit, then more rounds (capacity x rounds grows by >= 1.25 per attempt)
+            const double need = 1.25 * (double)S.h_counters.p[13] * S.cand_rounds;
+            const uint64_t lim = cand_limit();
+            S.cand_cap = (uint64_t)std::min<double>((double)lim, need);
+            S.cand_rounds = (uint32_t)std::max<double>(1.0, std::ceil(need / (double)S.cand_cap));
+            if (S.cand_rounds > splan.size() + splan_x.size())
+                throw Error(FPG_ENOMEM, "candidate buffer too small for one K2 tile (FPG_CAND_MAX_MB)");
+            redo = true;
+        }
+        if (S.h_counters.p[0] > S.out.cap) {  // reserved key slots did not fit
+            S.out_cap = S.h_counters.p[0] + S.h_counters.p[0] / 4 + 1024;
+            redo = true;
+        }
+        if (!redo) break;  // else grow and rescan
     }
+    S.cand_records = use_slice ? S.h_counters.p[13] : 0;
     S.total = S.h_counters.p[5];
     S.survivors = S.h_counters.p[1];
     S.candidates = S.h_counters.p[3];
@@ -1147,6 +1256,14 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
     S.run_ms = ms;
     CK(cudaEventElapsedTime(&ms, S.ev[1], S.ev[2]));
     S.filter_ms = ms;
+    S.verify_ms = 0;
+    if (use_slice) {  // K2 time = the rounds' time minus their K3 launches
+        for (uint32_t r = 0; r < S.cand_rounds; ++r) {
+            CK(cudaEventElapsedTime(&ms, S.ev_k3[2 * r], S.ev_k3[2 * r + 1]));
+            S.verify_ms += ms;
+        }
+        S.filter_ms -= S.verify_ms;
+    }
     g_launches += S.launches;
 }
 
@@ -1888,6 +2005,17 @@ int fpg_batch_last_candidates(const fpg_batch* batch, int32_t shard, uint64_t* c
     return guarded([&] {
         if (!batch || !candidates || shard < 0 || (size_t)shard >= batch->sb.size()) throw Error(FPG_EINVAL, "bad shard");
         *candidates = batch->sb[(size_t)shard]->candidates;
+    });
+}
+
+int fpg_batch_last_verify(const fpg_batch* batch, int32_t shard, double* verify_ms, uint64_t* records,
+                          uint32_t* rounds) {
+    return guarded([&] {
+        if (!batch || shard < 0 || (size_t)shard >= batch->sb.size()) throw Error(FPG_EINVAL, "bad shard");
+        const ShardBatch& S = *batch->sb[(size_t)shard];
+        if (verify_ms) *verify_ms = S.verify_ms;
+        if (records) *records = S.cand_records;
+        if (rounds) *rounds = S.cand_rounds;
     });
 }
 

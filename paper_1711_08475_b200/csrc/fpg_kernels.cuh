@@ -642,4 +642,5 @@ __global__ void k_merge_rows(const __grid_constant__ MergeParts mp, uint64_t nq,
 }  // namespace fpg
 
 #include "fpg_scan.cuh"
+#include "fpg_verify.cuh"
 #include "fpg_slice.cuh"

@@ -50,10 +50,11 @@
 // counters as they stand after the scheme planes (the reference's F_D alone).
 //
 // Candidates (rare) go to a lane-private queue in shared memory as
-// (query, slab, 32-bit word mask) and are byte-verified at k <= 1
-// (edit_distance.hpp:18-64) in warp-wide batches; matches leave as
-// (query id << 32 | sorted word position) keys through per-warp output
-// chunks (OutChunk) for K4, which maps positions to input-order ids.
+// (query, slab row, 32-bit word mask) and leave the kernel as records of the
+// candidate buffer; K3 (k_verify, fpg_verify.cuh) byte-verifies them at
+// k <= 1 (edit_distance.hpp:18-64) right behind K2 and emits the matches as
+// (query id << 32 | sorted word position) keys for K4, which maps positions
+// to input-order ids.
 #pragma once
 
 #include <cstdint>
@@ -79,7 +80,6 @@ constexpr int kSliceThreads = 256;
 constexpr int kSliceWarps = kSliceThreads / 32;
 constexpr int kSliceQ = 128;      // queries per tile (shared-memory masks)
 constexpr int kSliceCap = 8;      // queue entries per lane
-constexpr int kSliceWarpBuf = 256;  // expanded candidates per warp and verify round
 
 __host__ __device__ constexpr int slice_slabs_per_lane(int npt) { return npt <= 40 ? 2 : 1; }
 // Slabs per slab group: the unit a warp claims inside a tile (32 per lane row).
@@ -87,7 +87,7 @@ __host__ __device__ constexpr int slice_group_slabs(int npt) { return 32 * slice
 
 struct SliceTile {
     uint32_t slab_begin;   // first slab of the tile, bucket-local
-    uint32_t n_slabs;      // slabs in the tile (<= 256 * SL)
+    uint32_t n_slabs;      // slabs in the tile (a multiple of the slab group but for a bucket's last tile)
     uint32_t q_begin;      // sorted query positions [q_begin, q_begin + q_count)
     uint32_t q_count;
     uint64_t plane_base;   // u32 offset of the bucket's planes
@@ -106,23 +106,13 @@ struct SliceParams {
     const uint32_t* planes;     // dictionary planes
     const uint64_t* q_fp;       // query fingerprints (sorted order)
     const uint32_t* q_sigp;     // query sig' codes
+    const uint32_t* q_ids;
     const uint16_t* q_len;      // query lengths (sorted order)
     const uint32_t* q_start;    // per length: first sorted position
     const uint64_t* q_bbase;    // per length: byte offset in the padded query blob
-    const uint8_t* q_bytes;
-    const uint32_t* q_ids;
-    const uint8_t* w_bytes;
-    const uint32_t* w_ids;
-    uint64_t id_base;
     uint32_t* q_survivors;
-    unsigned long long* out;
-    unsigned long long* out_count;    // key slots reserved (OutChunk)
-    unsigned long long* match_total;
     unsigned long long* survivors_total;
     unsigned int* tile_counter;
-    unsigned long long* candidates;  // pairs handed to the byte verifier
-    uint32_t* q_matches;             // per input query: matches (K4 segment sizes)
-    uint64_t out_cap;
     int32_t k;
     int32_t stats;
     int32_t use_fp;             // scheme fields bound this metric (variant_supports, fingerprint.hpp:36-38)
@@ -133,6 +123,11 @@ struct SliceParams {
     unsigned long long* scanned;  // pairs actually evaluated (after the weight skip)
     int32_t exhaustive;         // verify every pair: no fingerprint / sig' pruning (naive-path timing)
     int32_t drop_candidates;    // A/B diagnosis only (FPG_DROP_CANDIDATES=1): queued candidates are discarded unverified
+    // candidate records for K3 (fpg_verify.cuh): cand_count = records reserved
+    // (past cand_cap they are dropped and the host reruns)
+    uint4* cand;
+    unsigned long long* cand_count;
+    uint64_t cand_cap;
 };
 
 __device__ __forceinline__ int stride_of_len(int len) { return len <= 16 ? 16 : (len + 15) & ~15; }
@@ -188,8 +183,7 @@ struct SliceShape {
 
 // Dynamic shared memory of k_slice<NP, .., S>.
 __host__ __device__ constexpr size_t slice_smem_bytes(int npt) {
-    return (size_t)kSliceQ * npt * 8 + 32u * kSliceQ + 8u * kSliceQ + 8u * kSliceCap * kSliceThreads +
-           4u * kSliceWarpBuf * kSliceWarps + 2u * kSliceQ * kSliceWarps;
+    return (size_t)kSliceQ * npt * 8 + 12u * kSliceQ + 8u * kSliceCap * kSliceThreads + 2u * kSliceQ * kSliceWarps;
 }
 
 // HOT: the options of the common run fixed at compile time (fingerprint
@@ -215,21 +209,18 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
     const int o_k = HOT ? 1 : P.k;
     extern __shared__ __align__(16) uint8_t smem[];
     uint2* s_qm = reinterpret_cast<uint2*>(smem);                           // [kSliceQ][NPT] (s, m)
-    uint4* s_qb = reinterpret_cast<uint4*>(s_qm + kSliceQ * NPT);           // [kSliceQ][2]: bytes 0..31
-    uint32_t* s_qinfo = reinterpret_cast<uint32_t*>(s_qb + 2 * kSliceQ);    // [kSliceQ]: length
-    uint32_t* s_qid = s_qinfo + kSliceQ;                                    // [kSliceQ]: input query id
-    uint2* s_queue = reinterpret_cast<uint2*>(s_qid + kSliceQ);             // [cap][threads]
-    uint32_t* s_wbuf = reinterpret_cast<uint32_t*>(s_queue + kSliceCap * kSliceThreads);  // [warps][buf]
-    uint16_t* s_qlist = reinterpret_cast<uint16_t*>(s_wbuf + kSliceWarpBuf * kSliceWarps);  // [warps][kSliceQ]
+    uint32_t* s_qid = reinterpret_cast<uint32_t*>(s_qm + kSliceQ * NPT);    // [kSliceQ]: input query id
+    uint32_t* s_qoff = s_qid + kSliceQ;                                     // [kSliceQ]: byte offset / 16 in the query blob
+    uint32_t* s_qlen = s_qoff + kSliceQ;                                    // [kSliceQ]: length
+    uint2* s_queue = reinterpret_cast<uint2*>(s_qlen + kSliceQ);            // [cap][threads]
+    uint16_t* s_qlist = reinterpret_cast<uint16_t*>(s_queue + kSliceCap * kSliceThreads);  // [warps][kSliceQ]
     __shared__ uint32_t s_grp;  // next slab group of the tile
     __shared__ uint32_t s_next[2];  // next tile index, double-buffered by iteration parity
     __shared__ uint32_t s_surv[kSliceQ];
     __shared__ uint32_t s_qw[2][kSliceQ];  // query group weights: even, odd nibbles (byte vectors)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     unsigned long long surv_warp = 0;  // lanes 0, 1: the warp's fingerprint survivors
-    uint32_t cand_lane = 0;
     unsigned long long scanned_warp = 0;  // lane 0
-    OutChunk oc;
 
     if (tid == 0) s_next[0] = atomicAdd(P.tile_counter, 1u);
     __syncthreads();
@@ -238,16 +229,11 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
         const SliceTile tl = tiles[t];
         if (tid == 0) s_next[it & 1] = atomicAdd(P.tile_counter, 1u);  // read after the end-of-tile barrier
 
-        // query (s, m) masks, verifier bytes / lengths / ids; one query per thread
+        // query (s, m) masks, ids and group weights; one query per thread
         for (uint32_t j = tid; j < tl.q_count; j += kSliceThreads) {
             const uint32_t qp = tl.q_begin + j;
             const uint64_t f = __ldg(P.q_fp + qp);
             const uint32_t g = __ldg(P.q_sigp + qp);
-            const int m = P.q_len[qp];
-            const int qs = stride_of_len(m);
-            const uint4* qb = reinterpret_cast<const uint4*>(P.q_bytes + P.q_bbase[m] + (uint64_t)(qp - P.q_start[m]) * qs);
-            const uint4 b0 = __ldg(qb);
-            const uint4 b1 = qs > 16 ? __ldg(qb + 1) : make_uint4(0, 0, 0, 0);
             const uint32_t id = P.q_ids[qp];
             uint2* dst = s_qm + j * NPT;
 #pragma unroll
@@ -255,10 +241,10 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 const uint32_t bit = b < NP ? (uint32_t)(f >> b) & 1u : (g >> (b - NP)) & 1u;
                 dst[b] = bit ? make_uint2(0xffffffffu, 0xffffffffu) : make_uint2(1u, 0u);
             }
-            s_qb[2 * j] = b0;
-            s_qb[2 * j + 1] = b1;
-            s_qinfo[j] = (uint32_t)m;
             s_qid[j] = id;
+            const int m = P.q_len[qp];
+            s_qlen[j] = (uint32_t)m;
+            s_qoff[j] = (uint32_t)((P.q_bbase[m] + (uint64_t)(qp - P.q_start[m]) * stride_of_len(m)) >> 4);
             s_surv[j] = 0u;
             const uint32_t qw = o_wskip ? P.q_weight[qp] : 0u;
             s_qw[0][j] = qw & kNib;
@@ -306,113 +292,40 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
         uint32_t qn = 0;  // queued entries of this lane
         const bool verify = !tl.count_only;
 
-        // Byte-verifies the warp's queued candidates.  The lanes' (query, slab,
-        // mask) entries are first expanded into a warp-wide list of single
-        // (query, word) candidates (rounds of <= kSliceWarpBuf), which the 32
-        // lanes then verify side by side, one candidate each.
-        uint32_t* wbuf = s_wbuf + warp * kSliceWarpBuf;
+        // Hands the warp's queued (query, slab row, mask) entries to K3
+        // (fpg_verify.cuh): the lanes' entries become self-describing records
+        // in the candidate buffer, reserved with one atomic per flush.  A
+        // reservation past the buffer's end is dropped: the count tells the
+        // host, which reruns the batch with a larger buffer or in more rounds.
         auto flush = [&]() {
             __syncwarp();
             if (P.drop_candidates) {
                 qn = 0;
                 return;
             }
-            for (;;) {
-                // pending candidate bits of this lane
-                uint32_t c = 0;
-                for (uint32_t s = 0; s < qn; ++s) c += __popc(s_queue[s * kSliceThreads + tid].y);
-                uint32_t incl = c;
+            uint32_t incl = qn;
 #pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
-                    if (lane >= d) incl += v;
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += v;
+            }
+            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+            if (total == 0) return;
+            unsigned long long base = 0;
+            if (lane == 31) base = atomicAdd(P.cand_count, (unsigned long long)total);
+            base = __shfl_sync(0xffffffffu, base, 31);
+            if (base + total <= P.cand_cap) {
+                uint4* dst = P.cand + base + (incl - qn);
+                // byte offset / 16 of word 0 of this lane's slab in tile slab row 0,
+                // and of one slab row (1024 words)
+                const uint32_t s16 = (uint32_t)tl.w_stride >> 4;
+                const uint32_t w0 = (uint32_t)(tl.w_bytes >> 4) + 32u * (tl.slab_begin + (uint32_t)lane) * s16;
+                for (uint32_t s = 0; s < qn; ++s) {
+                    const uint2 e = s_queue[s * kSliceThreads + tid];
+                    const uint32_t j = e.x & 0xffffu;
+                    FPG_CHECK(j < tl.q_count && 32u * (e.x >> 16) < tl.n_slabs);
+                    dst[s] = make_uint4(s_qoff[j], w0 + 1024u * s16 * (e.x >> 16), e.y, (uint32_t)tl.w_len | (s_qlen[j] << 16));
                 }
-                const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-                if (total == 0) break;
-                // this lane's candidates take ranks [incl - c, incl); those < kSliceWarpBuf go now
-                uint32_t rank = incl - c;
-                for (uint32_t s = 0; s < qn && rank < (uint32_t)kSliceWarpBuf; ++s) {
-                    uint2 e = s_queue[s * kSliceThreads + tid];
-                    const uint32_t j = e.x & 0xffffu, row = e.x >> 16;  // tile query, tile slab row
-#ifdef FPG_DEBUG
-                    if (!(j < tl.q_count && 32u * row < tl.n_slabs))
-                        printf("bad entry: j %u q_count %u row %u n_slabs %u y %x s %u qn %u tile %u\n", j, tl.q_count, row,
-                               tl.n_slabs, e.y, s, qn, t);
-#endif
-                    FPG_CHECK(j < tl.q_count && 32u * row < tl.n_slabs);
-                    const uint32_t wt0 = 32u * (32u * row + (uint32_t)lane);  // word index within the tile
-                    while (e.y && rank < (uint32_t)kSliceWarpBuf) {
-                        const int i = __ffs(e.y) - 1;
-                        e.y &= e.y - 1;
-                        wbuf[rank++] = (j << 25) | (wt0 + (uint32_t)i);
-                    }
-                    s_queue[s * kSliceThreads + tid].y = e.y;
-                }
-                __syncwarp();
-                const uint32_t m_all = min(total, (uint32_t)kSliceWarpBuf);
-                cand_lane += (lane == 0) ? m_all : 0u;
-                // two candidates per lane per round: both words' bytes are
-                // requested before either is compared (memory-level parallelism)
-                for (uint32_t base = 0; base < m_all; base += 64) {
-                    uint32_t jj[2], wi[2], bw[2][8];
-                    int mm[2];
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const uint32_t idx = base + 32u * u + lane;
-                        jj[u] = 0; wi[u] = 0; mm[u] = -1;
-#pragma unroll
-                        for (int c = 0; c < 8; ++c) bw[u][c] = 0u;
-                        if (idx < m_all) {
-                            const uint32_t v = wbuf[idx];
-                            jj[u] = v >> 25;
-                            wi[u] = 32u * tl.slab_begin + (v & 0x1ffffffu);
-                            FPG_CHECK(jj[u] < tl.q_count && wi[u] < tl.w_count);
-                            mm[u] = (int)s_qinfo[jj[u]];
-                            const int mx = mm[u] > tl.w_len ? mm[u] : tl.w_len;
-                            if (mx <= 32) load_padded<8>(P.w_bytes + tl.w_bytes + (uint64_t)wi[u] * tl.w_stride, tl.w_stride, bw[u]);
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        bool hit = false;
-                        const uint32_t j = jj[u], widx = wi[u];
-                        if (mm[u] >= 0) {
-                            const int m = mm[u], n = tl.w_len;
-                            const int mx = m > n ? m : n;
-                            if (mx <= 16) {
-                                uint32_t a4[4], b4[4];
-                                const uint4 qa = s_qb[2 * j];
-                                a4[0] = qa.x; a4[1] = qa.y; a4[2] = qa.z; a4[3] = qa.w;
-                                b4[0] = bw[u][0]; b4[1] = bw[u][1]; b4[2] = bw[u][2]; b4[3] = bw[u][3];
-                                hit = verify_regs<4>(a4, b4, m, n, o_k);
-                            } else if (mx <= 32) {
-                                uint32_t a8[8];
-                                const uint4 qa = s_qb[2 * j], qc = s_qb[2 * j + 1];
-                                a8[0] = qa.x; a8[1] = qa.y; a8[2] = qa.z; a8[3] = qa.w;
-                                a8[4] = qc.x; a8[5] = qc.y; a8[6] = qc.z; a8[7] = qc.w;
-                                hit = verify_regs<8>(a8, bw[u], m, n, o_k);
-                            } else {
-                                const uint32_t qpos = tl.q_begin + j;
-                                const int qs = stride_of_len(m);
-                                const uint8_t* qb = P.q_bytes + P.q_bbase[m] + (uint64_t)(qpos - P.q_start[m]) * qs;
-                                const uint8_t* wb = P.w_bytes + tl.w_bytes + (uint64_t)widx * tl.w_stride;
-                                hit = verify_pair(qb, m, qs, wb, n, tl.w_stride, o_k);
-                            }
-                        }
-                        const uint32_t hb = __ballot_sync(0xffffffffu, hit);
-                        if (hb) {
-                            const uint32_t qid = s_qid[j];
-                            const bool head = match_run_head(hit, qid, hb);
-                            const uint32_t heads = __ballot_sync(0xffffffffu, head);
-                            // sorted position; K4 maps it to the input-order id
-                            const uint64_t wid = hit ? (uint64_t)(tl.w_start + widx) : 0;
-                            oc.emit(hb, hit, ((uint64_t)qid << 32) | wid, P.out, P.out_cap, P.out_count);
-                            if (hit) count_match(P.q_matches, qid, hb, head, heads);
-                        }
-                    }
-                }
-                __syncwarp();
-                if (total <= (uint32_t)kSliceWarpBuf) break;
             }
             qn = 0;
         };
@@ -634,11 +547,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
         t = s_next[it & 1];
     }
     if (o_stats && lane < 2 && surv_warp) atomicAdd(P.survivors_total, surv_warp);
-    oc.close(P.out, P.out_cap);
-    if (lane == 0 && oc.real) atomicAdd(P.match_total, (unsigned long long)oc.real);
     if (lane == 0 && scanned_warp) atomicAdd(P.scanned, scanned_warp);
-    cand_lane = __reduce_add_sync(0xffffffffu, cand_lane);
-    if (lane == 0 && cand_lane) atomicAdd(P.candidates, (unsigned long long)cand_lane);
 }
 
 // ---------------------------------------------------------------- K1b planes

@@ -270,6 +270,32 @@ def test_output_regrowth_many_matches(oracle):
     assert_same(csr, st, *oracle.query_batch(blob, offs, qblob, qoffs, osch(s), Metric.Levenshtein, 1, True, True))
 
 
+@pytest.mark.parametrize("limit", [5000, 60_000])
+def test_candidate_buffer_rounds(oracle, monkeypatch, limit):
+    """K2 hands its candidates to K3 through a bounded record buffer.  With
+    the buffer limited to a few thousand records (FPG_CAND_MAX) the run
+    overflows, is redone with a grown buffer and then in several K2 + K3
+    rounds; results and QueryStats must not change."""
+    monkeypatch.setenv("FPG_CAND_MAX", str(limit))
+    blob, offs = generate_dictionary(3, n=150_000)
+    qb2, qo2 = generate_queries(3, blob, offs, nq=300)
+    pats = [b"e", b"ea", b"th", b"and"]
+    qblob, qoffs = pack(pats + [bytes(qb2[int(qo2[i]):int(qo2[i + 1])]) for i in range(300)])
+    s = make_scheme(blob, Variant.Occurrence, 16)
+    with GpuFingerprintedDictionary((blob, offs), s) as d:
+        b = d.batch()
+        b.upload(qblob, qoffs)
+        for metric in (Metric.Hamming, Metric.Levenshtein):
+            b.run(QueryOptions(metric, 1, True, True), want_stats=True)
+            t = b.timing()
+            csr, st = b.download()
+            assert t["candidate_records"] <= limit
+            if limit < 60_000:
+                assert t["verify_rounds"] > 1
+            assert_same(csr, st, *oracle.query_batch(blob, offs, qblob, qoffs, osch(s), metric, 1, True, True))
+        b.close()
+
+
 def test_k4_segment_size_classes(oracle, exact_path):
     """K4 sorts each query's matches by word id in one of three ways: <= 32
     (warp bitonic), 33..4096 (one CTA, shared-memory bitonic) and larger
