@@ -67,9 +67,9 @@ inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 // candidates, big segment flag, matches, pairs evaluated after the weight skip,
 // segments listed for k_seg_sort_big, its bucket overflow flag, the exact
 // path's tile counter and its pairs evaluated, candidate records reserved in
-// the current K2 round, the candidate buffer's overflow flag and the largest
-// per-round record count
-constexpr int kNumCounters = 14;
+// the current K2 round, the candidate buffer's overflow flag, the largest
+// per-round record count and K3's chunk cursor
+constexpr int kNumCounters = 15;
 constexpr unsigned kScatterBlocks = 148 * 4;  // grid-stride K4 scatter (the count is only known on the device)
 inline int stride_of(int len) { return len <= 16 ? 16 : (len + 15) & ~15; }
 
@@ -1070,20 +1070,20 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
     S.big_list.reserve(nq);
     const bool warp_sort = nq != 0;
     // Candidate buffer of the bit-sliced path: records per K2 + K3 round.
-    // FPG_CAND_MAX_MB bounds it (default 16 GB, and a quarter of the free
+    // FPG_CAND_MAX_MB bounds it (default 48 GB, and a third of the free
     // device memory); FPG_CAND_MAX (records) is the tests' override.
     auto cand_limit = [&]() -> uint64_t {
         size_t free_b = 0, total_b = 0;
         CK(cudaMemGetInfo(&free_b, &total_b));
-        const double mb = env_double("FPG_CAND_MAX_MB", 16384.0);
-        uint64_t rec = (uint64_t)std::min<double>(mb * 1048576.0, (double)(free_b + S.cand.cap * sizeof(uint4)) / 4.0) /
+        const double mb = env_double("FPG_CAND_MAX_MB", 49152.0);
+        uint64_t rec = (uint64_t)std::min<double>(mb * 1048576.0, (double)(free_b + S.cand.cap * sizeof(uint4)) / 3.0) /
                        sizeof(uint4);
         const double forced = env_double("FPG_CAND_MAX", 0.0);
         if (forced > 0) rec = (uint64_t)forced;
         return std::max<uint64_t>(rec, 1024);
     };
     if (use_slice && !S.cand_cap) {
-        S.cand_cap = std::min<uint64_t>(std::max<uint64_t>(executed / 64, 1u << 20), cand_limit());
+        S.cand_cap = std::min<uint64_t>(std::max<uint64_t>(executed / 256, 1u << 20), cand_limit());
         S.cand_rounds = 1;
     }
     for (bool first = true;; first = false) {
@@ -1106,29 +1106,26 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
                 CK(cudaEventCreate(&e));
                 S.ev_k3.push_back(e);
             }
-            // round r scans tiles [cut(pl, r), cut(pl, r + 1)) of each plan: equal shares of its work
-            auto cut = [&](const std::vector<fpg::SliceTile>& pl, uint32_t r) -> uint32_t {
-                if (r == 0) return 0;
-                if (r >= R) return (uint32_t)pl.size();
-                uint64_t work = 0, acc = 0;
-                for (const auto& t : pl) work += (uint64_t)t.q_count * t.n_slabs;
-                uint32_t i = 0;
-                for (; i < pl.size() && acc * R < work * r; ++i) acc += (uint64_t)pl[i].q_count * pl[i].n_slabs;
-                return i;
+            // round r scans every R-th tile of each plan from tile r on: the plan's
+            // mix of lengths (and so of candidates per tile) in every round
+            auto share = [&](const std::vector<fpg::SliceTile>& pl, uint32_t r) -> uint32_t {
+                return pl.size() > r ? (uint32_t)((pl.size() - r + R - 1) / R) : 0u;
             };
+            SP.tile_stride = R;
             for (uint32_t r = 0; r < R; ++r) {
                 if (r) {  // the rounds reuse the tile counters and the record buffer
                     CK(cudaMemsetAsync(S.counters.p + 2, 0, sizeof(unsigned long long), st));
                     CK(cudaMemsetAsync(S.counters.p + 9, 0, sizeof(unsigned long long), st));
                     CK(cudaMemsetAsync(S.counters.p + 11, 0, sizeof(unsigned long long), st));
+                    CK(cudaMemsetAsync(S.counters.p + 14, 0, sizeof(unsigned long long), st));
                 }
-                const uint32_t a0 = cut(splan, r), a1 = cut(splan, r + 1);
-                if (a1 > a0) {
-                    dispatch_slice(D->scheme, D->params.nsig, S.stiles.p + a0, a1 - a0, SP, st, sh.device);
+                SP.tile_off = r;
+                const uint32_t na = share(splan, r), nx = share(splan_x, r);
+                if (na) {
+                    dispatch_slice(D->scheme, D->params.nsig, S.stiles.p, na, SP, st, sh.device);
                     ++S.launches;
                 }
-                const uint32_t x0 = cut(splan_x, r), x1 = cut(splan_x, r + 1);
-                if (x1 > x0) {
+                if (nx) {
                     // the exact path: position-code planes instead of sig', own tile
                     // counter and pair count
                     fpg::SliceParams SX = SP;
@@ -1136,12 +1133,12 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
                     SX.q_sigp = Q.xc.p;
                     SX.tile_counter = reinterpret_cast<unsigned int*>(S.counters.p + 9);
                     SX.scanned = S.counters.p + 10;
-                    fpg_host::dispatch_slice_16x(field_width_of(D->scheme), S.stiles_x.p + x0, x1 - x0, SX, st, sh.device);
+                    fpg_host::dispatch_slice_16x(field_width_of(D->scheme), S.stiles_x.p, nx, SX, st, sh.device);
                     ++S.launches;
                 }
                 // K3 right behind: the record count stays on the device
                 CK(cudaEventRecord(S.ev_k3[2 * r], st));
-                if (a1 > a0 || x1 > x0) {
+                if (na || nx) {
                     // strings of up to 16 bytes compare from four registers each, else eight
                     // (Hamming only compares equal lengths)
                     const bool short16 = W.max_len <= 16 && (o.metric == FPG_HAMMING || Q.max_len <= 16);
@@ -1160,7 +1157,8 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
                     static const unsigned forced = (unsigned)env_double("FPG_VERIFY_CTAS", 0.0);
                     const unsigned vgrid = forced ? forced : (unsigned)resident[short16][dv];
                     kv<<<vgrid, fpg::kVerifyThreads, 0, st>>>(VP, S.cand.p, S.counters.p + 11, S.cand_cap, S.counters.p + 5,
-                                                              S.counters.p + 3, S.counters.p + 12, S.counters.p + 13);
+                                                              S.counters.p + 3, S.counters.p + 12, S.counters.p + 13,
+                                                              S.counters.p + 14);
                     CK(cudaGetLastError());
                     ++S.launches;
                 }
@@ -1216,6 +1214,17 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         if (!redo) break;  // else grow and rescan
     }
     S.cand_records = use_slice ? S.h_counters.p[13] : 0;
+    if (const char* dump = std::getenv("FPG_DUMP_CAND")) {  // diagnosis: the record stream's first 2^23 records
+        const uint64_t nr = std::min<uint64_t>(S.cand_records, S.cand_cap);
+        const uint64_t nd = std::min<uint64_t>(nr, 1ull << 21);
+        const uint64_t at = (uint64_t)((double)(nr - nd) * env_double("FPG_DUMP_AT", 0.0));
+        std::vector<uint4> h(nd);
+        CK(cudaMemcpy(h.data(), S.cand.p + at, nd * sizeof(uint4), cudaMemcpyDeviceToHost));
+        if (FILE* f = std::fopen(dump, "wb")) {
+            std::fwrite(h.data(), sizeof(uint4), nd, f);
+            std::fclose(f);
+        }
+    }
     S.total = S.h_counters.p[5];
     S.survivors = S.h_counters.p[1];
     S.candidates = S.h_counters.p[3];

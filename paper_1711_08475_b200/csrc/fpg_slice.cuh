@@ -128,6 +128,9 @@ struct SliceParams {
     uint4* cand;
     unsigned long long* cand_count;
     uint64_t cand_cap;
+    // the launch scans tiles tile_off + i * tile_stride, i < ntiles (round r of
+    // R takes every R-th tile, so every round sees the plan's mix of lengths)
+    uint32_t tile_off, tile_stride;
 };
 
 __device__ __forceinline__ int stride_of_len(int len) { return len <= 16 ? 16 : (len + 15) & ~15; }
@@ -226,7 +229,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
     __syncthreads();
     uint32_t t = s_next[0];
     for (uint32_t it = 1; t < ntiles; ++it) {
-        const SliceTile tl = tiles[t];
+        const SliceTile tl = tiles[(uint64_t)t * P.tile_stride + P.tile_off];
         if (tid == 0) s_next[it & 1] = atomicAdd(P.tile_counter, 1u);  // read after the end-of-tile barrier
 
         // query (s, m) masks, ids and group weights; one query per thread

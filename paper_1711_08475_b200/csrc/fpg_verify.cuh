@@ -143,6 +143,7 @@ __device__ __forceinline__ void verify_records(const VerifyParams& V, uint4 ea, 
 }
 
 constexpr int kVerifyThreads = 256;
+constexpr int kVerifyChunk = 256;  // records a warp claims at a time
 
 #ifndef FPG_K2_TU  // defined once, in fpg_api.cu
 // n_records = records K2 reserved this round (may exceed cap: the excess was
@@ -154,7 +155,8 @@ __global__ void __launch_bounds__(kVerifyThreads, NW == 4 ? 4 : 3) k_verify(cons
                                                            uint64_t cap, unsigned long long* __restrict__ match_total,
                                                            unsigned long long* __restrict__ candidates,
                                                            unsigned long long* __restrict__ overflow,
-                                                           unsigned long long* __restrict__ peak) {
+                                                           unsigned long long* __restrict__ peak,
+                                                           unsigned long long* __restrict__ cursor) {
     const uint64_t used = *n_records;
     const uint64_t n = used < cap ? used : cap;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -162,25 +164,42 @@ __global__ void __launch_bounds__(kVerifyThreads, NW == 4 ? 4 : 3) k_verify(cons
         if (used > *peak) *peak = used;  // rounds are stream-ordered: no race
     }
     const int lane = threadIdx.x & 31;
-    const uint64_t warp = ((uint64_t)blockIdx.x * kVerifyThreads + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * kVerifyThreads) >> 5;
     OutChunk oc;
     uint32_t pairs = 0;
     const uint4 none = make_uint4(0u, 0u, 0u, 0u);
-    // 64 consecutive records per warp and step (streamed once), fetched a step ahead
-    auto fetch = [&](uint64_t b, uint4& ea, uint4& eb) {
+    constexpr uint64_t kNoBlock = ~0ull;
+    // The warps claim chunks of kVerifyChunk records from a shared cursor, in
+    // stream order, so that the records in flight on the whole GPU are one
+    // window of the stream whatever the warps' speeds: records of one K2
+    // moment concern one slab range, whose word bytes then stay in L2 (a
+    // static, strided split lets the warps drift hundreds of MB apart).
+    uint64_t chunk = kNoBlock;
+    int sub = kVerifyChunk / 64;
+    auto next_block = [&]() -> uint64_t {  // 64 records per warp and step
+        if (sub == kVerifyChunk / 64) {
+            unsigned long long c = 0;
+            if (lane == 0) c = atomicAdd(cursor, 1ull);
+            chunk = __shfl_sync(0xffffffffu, c, 0) * (uint64_t)kVerifyChunk;
+            sub = 0;
+        }
+        if (chunk >= n) return kNoBlock;
+        return chunk + 64u * (uint32_t)(sub++);
+    };
+    auto fetch = [&](uint64_t b, uint4& ea, uint4& eb) {  // streamed once
         ea = b + lane < n ? __ldcs(records + b + lane) : none;
         eb = b + 32 + lane < n ? __ldcs(records + b + 32 + lane) : none;
     };
     uint4 ea = none, eb = none;
-    uint64_t b = warp * 64;
-    if (b < n) fetch(b, ea, eb);
-    for (; b < n; b += nwarps * 64) {
+    uint64_t cur = next_block();
+    if (cur != kNoBlock) fetch(cur, ea, eb);
+    while (cur != kNoBlock) {
         uint4 na = none, nb = none;
-        if (b + nwarps * 64 < n) fetch(b + nwarps * 64, na, nb);
+        const uint64_t nxt = next_block();  // fetched a step ahead
+        if (nxt != kNoBlock) fetch(nxt, na, nb);
         verify_records<NW>(V, ea, eb, oc, pairs);
         ea = na;
         eb = nb;
+        cur = nxt;
     }
     oc.close(V.out, V.out_cap);
     if (lane == 0 && oc.real) atomicAdd(match_total, (unsigned long long)oc.real);
