@@ -412,17 +412,22 @@ def main():
     if not args.no_flush:
         flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev0}")
 
+    plan_ms = None
+
     def barrier():
         for dv in set(devices):
             torch.cuda.synchronize(dv)
         if world > 1:
             torch.distributed.barrier()
 
-    for _ in range(args.warmup):
+    for i in range(args.warmup):
         batch.run(opt, want_stats=True)
+        if i == 0:  # the first run built the tile plan; the later ones reuse it
+            plan_ms = max(batch.timing(s).get("plan_ms", 0.0) for s in range(nsh))
     clocks = Clocks(dev0)
     clocks.start()
     step_ms, shard_ms, filt_ms, ver_ms, launches = [], [], [], [], 0
+
     barrier()
     clocks.open()
     for _ in range(args.steps):
@@ -450,13 +455,18 @@ def main():
     qb_p, qo_p = pinned_copy(w.qblob), pinned_copy(w.qoffs)
     e2e = None
     if not args.no_e2e:
-        gather = []
+        gather, phases = [], []
         if world == 1:
             def e2e_step():
+                t0 = time.perf_counter()
                 batch.upload(qb_p, qo_p)  # H2D
+                t1 = time.perf_counter()
                 batch.run(opt, want_stats=True)
+                t2 = time.perf_counter()
                 out = batch.download()  # D2H + host gather of the shard rows + QueryStats
+                t3 = time.perf_counter()
                 gather.append(batch.host_ms()["assemble_ms"])
+                phases.append((1e3 * (t1 - t0), 1e3 * (t2 - t1), 1e3 * (t3 - t2)))
                 return out[0]
         else:
             cap = int(csr.offsets[-1]) if csr.offsets is not None else 0
@@ -470,10 +480,14 @@ def main():
                 out = _gather_merge(batch, h_out)  # NCCL gather, device merge, D2H on rank 0
                 gather.append((time.perf_counter() - t1) * 1e3)
                 return out
-        for _ in range(max(1, args.warmup)):
-            e2e_step()
+        # warm up exactly like the timed loop: the previous step's result stays
+        # alive while the next one is produced, so two sets of pinned result
+        # blocks rotate (a fresh 340 MB page-locked allocation costs ~170 ms)
+        last = None
+        for _ in range(max(2, args.warmup)):
+            last = e2e_step()
         barrier()
-        e2e_s, last = 0.0, None
+        e2e_s = 0.0
         for _ in range(args.steps):
             if flush is not None:
                 flush.zero_()
@@ -494,9 +508,23 @@ def main():
                "h2d_bytes_per_step": h2d * (world if world > 1 else 1), "d2h_bytes_per_step": d2h,
                "ms_per_step": 1e3 * e2e_s / args.steps,
                "gather_ms_per_step": statistics.mean(gather[-args.steps:]) if gather else None,
+               "phases_ms": ({k: statistics.mean(p[i] for p in phases[-args.steps:])
+                              for i, k in enumerate(("upload", "run", "download"))} if phases else None),
+               "download_ms_steps": [round(p[2], 2) for p in phases[-args.steps:]] if phases else None,
                "gather": ("host: libfpg.so concatenates the shard rows (fpg_batch_download)" if world == 1 else
                           "device: NCCL p2p of the ranks' CSRs to rank 0 + fpg_csr_merge_device, one D2H"),
                "l2": L2_NOTE}
+
+    # the reference's per-pattern call (query_into, dictionary.hpp:75-118)
+    # through the same C ABI: one batch round trip per pattern
+    single_ms = None
+    if world == 1 and not args.no_e2e:
+        pats = [bytes(w.qblob[int(w.qoffs[i]):int(w.qoffs[i + 1])]) for i in range(0, min(w.nq, 64), 4)]
+        d.query(pats[0], opt)
+        t0 = time.perf_counter()
+        for pat in pats:
+            d.query(pat, opt)
+        single_ms = 1e3 * (time.perf_counter() - t0) / len(pats)
 
     if rank != 0:
         return
@@ -558,6 +586,7 @@ def main():
         "verifier_candidates_per_step": sum(t["candidates"] for t in t_last),
         "matches_per_step": int(csr.offsets[-1]) if world == 1 else None,
         "shard_ms_per_step": [statistics.mean(s[i] for s in shard_ms) for i in range(nsh)],
+        "host_plan_ms": plan_ms, "single_query_ms": single_ms,
         "construction_s": build_s, "setup_s": w.setup_s,
         "construction": construction_roofline(d),
         "gpu_launches": launches,

@@ -205,9 +205,11 @@ int fpg_batch_last_candidates(const fpg_batch* batch, int32_t shard, uint64_t* c
  * the last run on `shard`: its CUDA-event time (filter_ms of
  * fpg_batch_last_timing excludes it), the largest number of 16-byte
  * candidate records one K2 round wrote, and the K2 + K3 rounds the run was
- * cut into (1 unless the records exceeded the buffer limit). */
+ * cut into (1 unless the records exceeded the buffer limit).  *plan_ms is
+ * the host time the shard's last fresh tile plan took to build (runs with
+ * the same query length histogram and options reuse the plan). */
 int fpg_batch_last_verify(const fpg_batch* batch, int32_t shard, double* verify_ms, uint64_t* records,
-                          uint32_t* rounds);
+                          uint32_t* rounds, double* plan_ms);
 /* Length-compatible pairs the last run on `shard` actually evaluated: the
  * executed pairs minus those skipped whole because their group weights are
  * more than 2k apart (L1 distance over 4 field groups <= F_D, so they are

@@ -93,7 +93,7 @@ FPG_SIGNATURES = {
                                              c_u64p]),
     "fpg_batch_last_candidates": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, c_u64p]),
     "fpg_batch_last_verify": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_double), c_u64p,
-                                             ctypes.POINTER(ctypes.c_uint32)]),
+                                             ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_double)]),
     "fpg_batch_last_scanned": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, c_u64p]),
     "fpg_batch_last_scanned_exact": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, c_u64p]),
     "fpg_batch_last_host_ms": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),

@@ -650,7 +650,7 @@ struct ShardBatch {
     HBuf<uint32_t> h_ids, h_qsurv;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     uint64_t total = 0, executed = 0, survivors = 0, candidates = 0, scanned = 0, scanned_x = 0, launches = 0;
-    double run_ms = 0, filter_ms = 0, verify_ms = 0;
+    double run_ms = 0, filter_ms = 0, verify_ms = 0, plan_ms = 0;
     uint64_t out_cap = 1 << 20;
     // K2 -> K3 candidate records (fpg_verify.cuh): capacity per round (0: sized
     // from the plan at first use) and the K2 + K3 rounds the tile plan is cut
@@ -819,6 +819,7 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
     const bool use_slice = D->slice && o.k <= 1;
     const bool from_slice = D->slice && !use_slice;  // generic kernel over bit-sliced collections
     const bool replan = !S.plan_valid || std::memcmp(&S.plan_opts, &o, sizeof(o)) != 0;
+    const auto plan_t0 = std::chrono::steady_clock::now();
     if (!replan) {
         executed = S.executed;
     } else if (use_slice) {
@@ -995,6 +996,9 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
     S.executed = executed;
     S.plan_valid = true;
     S.plan_opts = o;
+    // host time of building (and queueing the upload of) a fresh tile plan;
+    // later runs with the same length histogram and options reuse it
+    if (replan) S.plan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - plan_t0).count();
 
     fpg::ScanParams P{};
     fpg::SliceParams SP{};
@@ -1214,17 +1218,6 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         if (!redo) break;  // else grow and rescan
     }
     S.cand_records = use_slice ? S.h_counters.p[13] : 0;
-    if (const char* dump = std::getenv("FPG_DUMP_CAND")) {  // diagnosis: the record stream's first 2^23 records
-        const uint64_t nr = std::min<uint64_t>(S.cand_records, S.cand_cap);
-        const uint64_t nd = std::min<uint64_t>(nr, 1ull << 21);
-        const uint64_t at = (uint64_t)((double)(nr - nd) * env_double("FPG_DUMP_AT", 0.0));
-        std::vector<uint4> h(nd);
-        CK(cudaMemcpy(h.data(), S.cand.p + at, nd * sizeof(uint4), cudaMemcpyDeviceToHost));
-        if (FILE* f = std::fopen(dump, "wb")) {
-            std::fwrite(h.data(), sizeof(uint4), nd, f);
-            std::fclose(f);
-        }
-    }
     S.total = S.h_counters.p[5];
     S.survivors = S.h_counters.p[1];
     S.candidates = S.h_counters.p[3];
@@ -2018,11 +2011,12 @@ int fpg_batch_last_candidates(const fpg_batch* batch, int32_t shard, uint64_t* c
 }
 
 int fpg_batch_last_verify(const fpg_batch* batch, int32_t shard, double* verify_ms, uint64_t* records,
-                          uint32_t* rounds) {
+                          uint32_t* rounds, double* plan_ms) {
     return guarded([&] {
         if (!batch || shard < 0 || (size_t)shard >= batch->sb.size()) throw Error(FPG_EINVAL, "bad shard");
         const ShardBatch& S = *batch->sb[(size_t)shard];
         if (verify_ms) *verify_ms = S.verify_ms;
+        if (plan_ms) *plan_ms = S.plan_ms;
         if (records) *records = S.cand_records;
         if (rounds) *rounds = S.cand_rounds;
     });

@@ -613,13 +613,13 @@ class Batch:
         check(self._lib.fpg_batch_last_scanned(self._h, shard, ctypes.byref(scan)))
         scan_x = ctypes.c_uint64()
         check(self._lib.fpg_batch_last_scanned_exact(self._h, shard, ctypes.byref(scan_x)))
-        ver_ms, recs, rounds = ctypes.c_double(), ctypes.c_uint64(), ctypes.c_uint32()
+        ver_ms, recs, rounds, plan_ms = ctypes.c_double(), ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_double()
         check(self._lib.fpg_batch_last_verify(self._h, shard, ctypes.byref(ver_ms), ctypes.byref(recs),
-                                              ctypes.byref(rounds)))
+                                              ctypes.byref(rounds), ctypes.byref(plan_ms)))
         return {"run_ms": run_ms.value, "filter_ms": filt_ms.value, "executed_pairs": ex.value,
                 "survivors": sv.value, "launches": ln.value, "candidates": cand.value, "scanned_pairs": scan.value,
                 "scanned_pairs_exact": scan_x.value, "verify_ms": ver_ms.value, "candidate_records": recs.value,
-                "verify_rounds": rounds.value}
+                "verify_rounds": rounds.value, "plan_ms": plan_ms.value}
 
     def host_ms(self) -> dict:
         """Host-side ms of the last upload, download (D2H wait) and result

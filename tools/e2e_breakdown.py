@@ -14,6 +14,8 @@ from paper_1711_08475_b200 import GpuFingerprintedDictionary, QueryOptions  # no
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 cell = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+HOLD = len(sys.argv) > 3 and sys.argv[3] == "hold"
+held = None
 w = bench.Workload(cfg, cell)
 qb, qo = bench.pinned_copy(w.qblob), bench.pinned_copy(w.qoffs)
 opt = QueryOptions(w.metric, 1, True, True)
@@ -24,6 +26,8 @@ for it in range(8):
     t0 = time.perf_counter(); b.upload(qb, qo); t1 = time.perf_counter()
     b.run(opt, want_stats=True); t2 = time.perf_counter()
     out = b.download(); t3 = time.perf_counter()
+    if HOLD:
+        held = out  # like bench.py: the previous result stays alive during the next step
     del out
     if it >= 2:
         h = b.host_ms()
