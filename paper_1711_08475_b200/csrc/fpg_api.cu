@@ -474,7 +474,7 @@ struct Collection {
                 plane_base[L] = pb;
                 const uint64_t ns = cdiv(count[L], 32);
                 sl += ns;
-                pb += ns * (uint64_t)npt;
+                pb += cdiv(ns, 32) * 32 * (uint64_t)npt;  // whole rows of 32 slabs (fpg_slice.cuh layout)
             }
             slab_start[L1] = (uint32_t)sl;
             planes.reserve(pb);
@@ -523,7 +523,7 @@ struct Collection {
                 uint64_t xb = 0;
                 for (int L = 0; L <= fpg::kXLen; ++L) {
                     xplane_base[L] = xb;
-                    xb += cdiv(count[L], 32) * (uint64_t)xnpt;
+                    xb += cdiv(cdiv(count[L], 32), 32) * 32 * (uint64_t)xnpt;
                 }
                 const uint32_t xsl = slab_start[fpg::kXLen + 1];
                 if (xsl) {

@@ -7,9 +7,11 @@
 // Planes 0..NP-1 are the scheme fingerprint bits in the reference layout
 // (fingerprint.hpp:48-56, :138-147: NF fields of FW bits above EXTRA one-bit
 // fields); planes NP..NPT-1 are the "complement signature" sig' (below).
-// In HBM the planes of a bucket are plane-major: plane b of slab s at
-// plane_base + b * n_slabs + s, so lanes holding consecutive slabs load
-// coalesced 128-byte rows.
+// In HBM a bucket's slabs are grouped into rows of 32 consecutive slabs, the
+// unit a warp loads (lane = slab), and a row is plane-major: plane b of slab
+// s at plane_base + (s / 32) * NPT * 32 + b * 32 + s % 32.  A lane reads its
+// slab's NPT planes at compile-time offsets from one address, and every load
+// of the warp is one coalesced 128-byte line.
 //
 // Test.  The reference rejects a pair iff ceil(F_D / 2) > k, i.e. F_D > 2k
 // (dictionary.hpp:102-106, fingerprint.hpp:199,293-301), F_D = number of
@@ -270,14 +272,13 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 const uint32_t slab = tl.slab_begin + rel;
                 const bool ok = rel < tl.n_slabs;
                 // lanes past the tile's end load the tile's first slab (valid
-                // memory; valid[r] = 0 masks every result of theirs): one
-                // pointer step per plane, no per-plane predication
-                const uint32_t* src = planes + (ok ? slab : tl.slab_begin);
+                // memory; valid[r] = 0 masks every result of theirs).  Rows of
+                // 32 slabs are plane-major: one address per row, the planes at
+                // compile-time offsets
+                const uint32_t sl_ = ok ? slab : tl.slab_begin;
+                const uint32_t* src = planes + (uint64_t)(sl_ >> 5) * (NPT * 32) + (sl_ & 31u);
 #pragma unroll
-                for (int b = 0; b < NPT; ++b) {
-                    pl[r][b] = __ldg(src);
-                    src += tl.ns;
-                }
+                for (int b = 0; b < NPT; ++b) pl[r][b] = __ldg(src + 32 * b);
                 const uint32_t rem = tl.w_count - 32u * slab;  // words left in the bucket from this slab on
                 valid[r] = !ok ? 0u : rem >= 32u ? 0xffffffffu : ((1u << rem) - 1u);
                 vw += __popc(valid[r]);
@@ -323,6 +324,7 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                 // and of one slab row (1024 words)
                 const uint32_t s16 = (uint32_t)tl.w_stride >> 4;
                 const uint32_t w0 = (uint32_t)(tl.w_bytes >> 4) + 32u * (tl.slab_begin + (uint32_t)lane) * s16;
+#pragma unroll 1
                 for (uint32_t s = 0; s < qn; ++s) {
                     const uint2 e = s_queue[s * kSliceThreads + tid];
                     const uint32_t j = e.x & 0xffffu;
@@ -616,8 +618,8 @@ __global__ void __launch_bounds__(32 * kPlanesSlabs) k_planes(
         const uint32_t g = gs0 + (uint32_t)lane;
         if (g < total_slabs) {
             const int L = bucket(g);
-            const uint32_t ns = slab_start[L + 1] - slab_start[L];
-            planes[plane_base[L] + (uint64_t)b * ns + (g - slab_start[L])] = tile[b][lane];
+            const uint32_t sl = g - slab_start[L];  // row of 32 slabs, plane-major inside
+            planes[plane_base[L] + (uint64_t)(sl >> 5) * ((uint32_t)npt * 32u) + (uint32_t)b * 32u + (sl & 31u)] = tile[b][lane];
         }
     }
 }
