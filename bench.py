@@ -569,6 +569,8 @@ def main():
         gbs = ver_bytes / (ver_avg_ms * 1e6)
         verify = {"kernel": "k_verify (K3)", "bound": "hbm", "ms_per_step": ver_avg_ms, "algorithmic_bytes": ver_bytes,
                   "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm, "peak_basis": hbm_basis,
+                  "traffic": profiled_traffic(f"config{args.config}", w.cell_name() + " k_verify"),
+                  "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",
                   "candidate_records": t0s.get("candidate_records", 0), "rounds": t0s.get("verify_rounds", 1),
                   "bytes_basis": f"16 B per record (upper bound: records of the largest round x rounds) + {w_stride} B "
                                  "per candidate word (random 32-byte sectors in practice) + 8 B per match key"}

@@ -293,7 +293,11 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
         if (tid == 0) s_grp = (uint32_t)kSliceWarps;
         __syncthreads();
 
-        uint32_t qn = 0;  // queued entries of this lane
+        // The lane's queue is addressed by a running shared-memory pointer
+        // (32-bit window address): a push is one store and one add.
+        const uint32_t qbase = (uint32_t)__cvta_generic_to_shared(s_queue + tid);
+        constexpr uint32_t kQStep = 8u * kSliceThreads;  // bytes between a lane's slots
+        uint32_t qtop = qbase;  // next free slot
         const bool verify = !tl.count_only;
 
         // Hands the warp's queued (query, slab row, mask) entries to K3
@@ -303,10 +307,9 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
         // host, which reruns the batch with a larger buffer or in more rounds.
         auto flush = [&]() {
             __syncwarp();
-            if (P.drop_candidates) {
-                qn = 0;
-                return;
-            }
+            const uint32_t qn = (qtop - qbase) / kQStep;  // queued entries of this lane
+            qtop = qbase;
+            if (P.drop_candidates) return;
             uint32_t incl = qn;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
@@ -332,7 +335,6 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                     dst[s] = make_uint4(s_qoff[j], w0 + 1024u * s16 * (e.x >> 16), e.y, (uint32_t)tl.w_len | (s_qlen[j] << 16));
                 }
             }
-            qn = 0;
         };
 
         // Per-warp slab count: warps whose second slab row is empty (a
@@ -489,12 +491,14 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
                     for (int r = 0; r < SLX; ++r) {
                         const uint32_t cand = X ? exact_pass(h, r) : o_exhaustive ? valid[r] : passed(h, r);
                         if (cand) {
-                            s_queue[qn * kSliceThreads + tid] = make_uint2(jq[h] | ((row0 + (uint32_t)r) << 16), cand);
-                            ++qn;
+                            asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(qtop), "r"(jq[h] | ((row0 + (uint32_t)r) << 16)),
+                                         "r"(cand)
+                                         : "memory");
+                            qtop += kQStep;
                         }
                     }
                 // room for the largest step (2 queries x SL slabs) whatever comes next
-                if (__any_sync(0xffffffffu, qn > (uint32_t)(kSliceCap - 2 * SL))) flush();
+                if (__any_sync(0xffffffffu, qtop > qbase + (uint32_t)(kSliceCap - 2 * SL) * kQStep)) flush();
             }
 #undef FPG_QS
 #undef FPG_QM

@@ -12,9 +12,8 @@ for k in ${KERNELS:-k_verify k_slice}; do
   python tools/ncu_summary.py sass $o/$k.ncu-rep > $o/${k}_sass.txt 2>&1
   ncu -i $o/$k.ncu-rep --page details --csv 2>/dev/null | gzip > $o/${k}_details.csv.gz
   ncu -i $o/$k.ncu-rep --page raw --csv 2>/dev/null | gzip > $o/${k}_raw.csv.gz
-  if [ $k = k_slice ]; then
-    key=$(python -c "import bench; w=bench.Workload.__new__(bench.Workload); w.cfg, w.cell = $cfg, $cell; print('config$cfg', w.cell_name())")
-    python tools/ncu_summary.py traffic $o/$k.ncu-rep "$key" $o/traffic.json > /dev/null 2>&1
-  fi
+  key=$(python -c "import bench; w=bench.Workload.__new__(bench.Workload); w.cfg, w.cell = $cfg, $cell; print('config$cfg', w.cell_name())")
+  [ $k = k_verify ] && key="$key k_verify"
+  python tools/ncu_summary.py traffic $o/$k.ncu-rep "$key" $o/traffic.json > /dev/null 2>&1
   rm -f $o/$k.ncu-rep
 done
