@@ -14,12 +14,13 @@
 // edit_distance.hpp:18-64) at high occupancy.  A record names its bytes
 // directly, so the dependent chain is record -> (query bytes, word bytes) ->
 // compare; the tables that turn offsets back into a query id and a sorted
-// word position are only read for hits.  Each lane holds two records and the
-// warp verifies up to two candidates per lane and round, all their bytes
-// requested before any is compared; the next records are fetched a round
-// ahead.  Hits leave as (query id << 32 | sorted word position) keys through
-// the per-warp output chunks K4 reads.  The kernel is bound by the random
-// 16-byte word reads (32-byte DRAM sectors), not by arithmetic.
+// word position are only read for hits.  A warp takes 64 records at a time,
+// lists their candidates in shared memory and verifies 64 per round, two per
+// lane, all their bytes requested before any is compared; the next records
+// are fetched a step ahead.  Hits leave as (query id << 32 | sorted word
+// position) keys through the per-warp output chunks K4 reads.  The warps
+// claim their records in stream order, which keeps the word bytes of the
+// records in flight in L2; the kernel then is bound by instruction issue.
 //
 // The buffer has a fixed capacity per K2 launch.  Records reserved past its
 // end are dropped and counted; k_verify raises the run's overflow flag and
@@ -76,34 +77,58 @@ __device__ __forceinline__ bool hamming_regs(const uint32_t (&q)[NW], const uint
 
 // Warp-collective.  Every lane brings two records (z = 0: none); strings of
 // up to 4 NW bytes are compared from registers, longer ones from memory.
+// The 64 records' candidates (one per mask bit) are first listed in shared
+// memory in lane order, so that every round verifies 64 of them, two per
+// lane, whatever the lanes' own counts (a lane-private loop over its masks
+// ran 2.9 rounds per 64 records on config 5 where the list needs 1.4).
+// s_rec: the warp's 64 records, s_list: <= 2048 entries (record << 5 | bit).
 // `pairs` accumulates the lane's candidate pairs (diagnostics).
 template <int NW>
-__device__ __forceinline__ void verify_records(const VerifyParams& V, uint4 ea, uint4 eb, OutChunk& oc, uint32_t& pairs) {
-    uint32_t ma = ea.z, mb = eb.z;
-    pairs += (uint32_t)(__popc(ma) + __popc(mb));
-    while (__any_sync(0xffffffffu, (ma | mb) != 0u)) {
-        int bit[2], len[2];         // len = word length | query length << 16
+__device__ __forceinline__ void verify_records(const VerifyParams& V, uint4 ea, uint4 eb, OutChunk& oc, uint32_t& pairs,
+                                               uint4* s_rec, uint16_t* s_list) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t ca = (uint32_t)__popc(ea.z), cb = (uint32_t)__popc(eb.z);
+    pairs += ca + cb;
+    uint32_t incl = ca + cb;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += v;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) return;
+    __syncwarp();  // the previous call's readers are done with s_rec / s_list
+    s_rec[lane] = ea;
+    s_rec[32 + lane] = eb;
+    {
+        uint32_t rank = incl - (ca + cb);
+        for (uint32_t mk = ea.z; mk; mk &= mk - 1) s_list[rank++] = (uint16_t)((lane << 5) | (__ffs(mk) - 1));
+        for (uint32_t mk = eb.z; mk; mk &= mk - 1) s_list[rank++] = (uint16_t)(((32 + lane) << 5) | (__ffs(mk) - 1));
+    }
+    __syncwarp();
+    for (uint32_t base = 0; base < total; base += 64) {
+        // two candidates per lane and round: all their bytes are requested
+        // before any is compared
+        bool have[2];
+        int len[2];                 // word length | query length << 16
         uint32_t qo[2], wo[2];      // byte offsets / 16 of the query and of the candidate word
         uint32_t qa[2][NW], bw[2][NW];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-            bit[u] = -1;
+            const uint32_t idx = base + 32u * u + (uint32_t)lane;
+            have[u] = idx < total;
             len[u] = 0;
             qo[u] = wo[u] = 0u;
 #pragma unroll
             for (int c = 0; c < NW; ++c) qa[u][c] = bw[u][c] = 0u;
-            if (ma | mb) {
-                const bool a = ma != 0u;
-                uint32_t mk = a ? ma : mb;
-                bit[u] = __ffs(mk) - 1;
-                mk &= mk - 1;
-                if (a) ma = mk;
-                else mb = mk;
-                len[u] = (int)(a ? ea.w : eb.w);
+            if (have[u]) {
+                const uint32_t e = s_list[idx];
+                const uint4 r = s_rec[e >> 5];
+                len[u] = (int)r.w;
                 const int n = len[u] & 0xffff, m = len[u] >> 16;
                 const int ws = verify_stride(n);
-                qo[u] = a ? ea.x : eb.x;
-                wo[u] = (a ? ea.y : eb.y) + (uint32_t)bit[u] * (uint32_t)(ws >> 4);
+                qo[u] = r.x;
+                wo[u] = r.y + (e & 31u) * (uint32_t)(ws >> 4);
                 if ((m > n ? m : n) <= 4 * NW) {
                     load_words<NW>(V.q_bytes + 16ull * qo[u], verify_stride(m), qa[u]);
                     load_words<NW>(V.w_bytes + 16ull * wo[u], ws, bw[u]);
@@ -112,9 +137,10 @@ __device__ __forceinline__ void verify_records(const VerifyParams& V, uint4 ea, 
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
+            if (u && base + 32u >= total) break;  // warp-uniform
             bool hit = false;
             const int n = len[u] & 0xffff, m = len[u] >> 16;
-            if (bit[u] >= 0) {
+            if (have[u]) {
                 if (m == n && n <= 4 * NW)
                     hit = hamming_regs<NW>(qa[u], bw[u], V.k);
                 else if ((m > n ? m : n) <= 4 * NW)
@@ -168,6 +194,10 @@ __global__ void __launch_bounds__(kVerifyThreads, NW == 4 ? 4 : 3) k_verify(cons
     uint32_t pairs = 0;
     const uint4 none = make_uint4(0u, 0u, 0u, 0u);
     constexpr uint64_t kNoBlock = ~0ull;
+    __shared__ __align__(16) uint4 s_rec_all[kVerifyThreads / 32][64];
+    __shared__ uint16_t s_list_all[kVerifyThreads / 32][64 * 32];
+    uint4* s_rec = s_rec_all[threadIdx.x >> 5];
+    uint16_t* s_list = s_list_all[threadIdx.x >> 5];
     // The warps claim chunks of kVerifyChunk records from a shared cursor, in
     // stream order, so that the records in flight on the whole GPU are one
     // window of the stream whatever the warps' speeds: records of one K2
@@ -196,7 +226,7 @@ __global__ void __launch_bounds__(kVerifyThreads, NW == 4 ? 4 : 3) k_verify(cons
         uint4 na = none, nb = none;
         const uint64_t nxt = next_block();  // fetched a step ahead
         if (nxt != kNoBlock) fetch(nxt, na, nb);
-        verify_records<NW>(V, ea, eb, oc, pairs);
+        verify_records<NW>(V, ea, eb, oc, pairs, s_rec, s_list);
         ea = na;
         eb = nb;
         cur = nxt;
