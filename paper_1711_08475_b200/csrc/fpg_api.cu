@@ -1101,7 +1101,17 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         }
         CK(cudaEventRecord(S.ev[1], st));
         if (use_slice) {
-            S.cand.reserve(S.cand_cap);
+            // a refused allocation (fragmented or shared device memory) halves the
+            // buffer; the run then takes more rounds instead of failing
+            while (S.cand.cap < S.cand_cap) {
+                try {
+                    S.cand.reserve(S.cand_cap);
+                } catch (const Error&) {
+                    cudaGetLastError();
+                    if (S.cand_cap <= (1u << 20)) throw;
+                    S.cand_cap = std::max<uint64_t>(S.cand_cap / 2, 1u << 20);
+                }
+            }
             SP.cand = S.cand.p;
             SP.cand_cap = S.cand_cap;
             const uint32_t R = S.cand_rounds;
@@ -1306,18 +1316,44 @@ void upload(fpg_batch* B, const uint8_t* qbytes, const uint64_t* qoffsets, uint6
     const int L1 = fpg::kMaxLen + 1;
     B->qcount.assign(L1, 0);
     const uint64_t q0 = nq ? qoffsets[0] : 0;
+    // Lengths, their histogram and (below) the stable counting sort run on up
+    // to 16 host threads over contiguous chunks of a large batch: chunk c
+    // scatters its queries behind those of the chunks before it.
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const uint64_t C = std::max<uint64_t>(1, std::min<uint64_t>(hw, nq >> 16));
+    auto chunk_lo = [&](uint64_t c) { return nq * c / C; };
+    auto chunks = [&](auto&& f) {
+        if (C == 1) {
+            f(uint64_t(0));
+            return;
+        }
+        std::vector<std::thread> th;
+        for (uint64_t c = 0; c < C; ++c) th.emplace_back([&f, c] { f(c); });
+        for (auto& x : th) x.join();
+    };
+    std::vector<uint64_t> cmax(C, 0);
+    std::vector<std::vector<uint32_t>> chist(C);
+    chunks([&](uint64_t c) {
+        std::vector<uint32_t>& h = chist[c];
+        h.assign(L1, 0);
+        uint64_t mx = 0;
+        for (uint64_t i = chunk_lo(c); i < chunk_lo(c + 1); ++i) {
+            const uint64_t len = qoffsets[i + 1] - qoffsets[i];  // wraps (huge) if not ascending
+            mx = len > mx ? len : mx;
+            B->qlen[i] = (uint32_t)len;
+            if (len < (uint64_t)L1) ++h[len];
+        }
+        cmax[c] = mx;
+    });
     uint64_t len_max = 0;
-    for (uint64_t i = 0; i < nq; ++i) {
-        const uint64_t len = qoffsets[i + 1] - qoffsets[i];  // wraps (huge) if not ascending
-        len_max = len > len_max ? len : len_max;
-        B->qlen[i] = (uint32_t)len;
-    }
+    for (uint64_t c = 0; c < C; ++c) len_max = std::max(len_max, cmax[c]);
     if (len_max > (uint64_t)fpg::kMaxLen) {
         for (uint64_t i = 0; i < nq; ++i)
             if (qoffsets[i + 1] < qoffsets[i]) throw Error(FPG_EINVAL, "query offsets not ascending");
         throw Error(FPG_EINVAL, "query longer than FPG_MAX_WORD_LEN");
     }
-    for (uint64_t i = 0; i < nq; ++i) ++B->qcount[B->qlen[i]];
+    for (uint64_t c = 0; c < C; ++c)
+        for (uint64_t L = 0; L <= len_max; ++L) B->qcount[L] += chist[c][L];
     if (nq && qoffsets[nq] > q0 && !qbytes) throw Error(FPG_EINVAL, "null query bytes");
     // Length buckets: stable counting sort of the query ids (the layout K1
     // writes, with the padded-byte offset of every bucket).
@@ -1344,8 +1380,18 @@ void upload(fpg_batch* B, const uint8_t* qbytes, const uint64_t* qoffsets, uint6
     std::fill(B->h_bbase.p + len_max + 1, B->h_bbase.p + L1, bpos);
     B->qtotal_bytes = bpos;
     {
-        std::vector<uint32_t> cur(B->qstart);
-        for (uint64_t i = 0; i < nq; ++i) B->h_order.p[cur[B->qlen[i]]++] = (uint32_t)i;
+        // chunk c's first slot per length: the bucket start plus the earlier chunks' counts
+        std::vector<uint32_t> run(B->qstart.begin(), B->qstart.begin() + len_max + 1);
+        for (uint64_t c = 0; c < C; ++c)
+            for (uint64_t L = 0; L <= len_max; ++L) {
+                const uint32_t n_cl = chist[c][L];
+                chist[c][L] = run[L];
+                run[L] += n_cl;
+            }
+        chunks([&](uint64_t c) {
+            std::vector<uint32_t>& cur = chist[c];
+            for (uint64_t i = chunk_lo(c); i < chunk_lo(c + 1); ++i) B->h_order.p[cur[B->qlen[i]]++] = (uint32_t)i;
+        });
     }
     const uint64_t nbytes = nq ? qoffsets[nq] - q0 : 0;
     const auto t1 = std::chrono::steady_clock::now();
