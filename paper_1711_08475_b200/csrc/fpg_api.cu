@@ -656,7 +656,7 @@ struct ShardBatch {
     // from the plan at first use) and the K2 + K3 rounds the tile plan is cut
     // into when one round's records would not fit
     DBuf<uint4> cand;
-    uint64_t cand_cap = 0, cand_records = 0;
+    uint64_t cand_cap = 0, cand_records = 0, cand_fail = 0;
     uint32_t cand_rounds = 1;
     std::vector<cudaEvent_t> ev_k3;  // per round: before / after k_verify
 };
@@ -1084,6 +1084,7 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
                        sizeof(uint4);
         const double forced = env_double("FPG_CAND_MAX", 0.0);
         if (forced > 0) rec = (uint64_t)forced;
+        if (S.cand_fail) rec = std::min<uint64_t>(rec, S.cand_fail / 2);  // an allocation of cand_fail records was refused
         return std::max<uint64_t>(rec, 1024);
     };
     if (use_slice && !S.cand_cap) {
@@ -1109,6 +1110,7 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
                 } catch (const Error&) {
                     cudaGetLastError();
                     if (S.cand_cap <= (1u << 20)) throw;
+                    S.cand_fail = S.cand_cap;  // bounds the later limits (cand_limit)
                     S.cand_cap = std::max<uint64_t>(S.cand_cap / 2, 1u << 20);
                 }
             }
