@@ -8,8 +8,8 @@ for cfg in 1 2 3 4 5; do
       > gpurun_out/sweep/c${cfg}_${cell}.log 2>&1
     echo "cfg=$cfg cell=$cell rc=$? $(tail -1 gpurun_out/sweep/c${cfg}_${cell}.log | python -c 'import sys,json
 try:
-  d=json.loads(sys.stdin.read()); r=d["roofline"]
-  print(d["config"]["cell"], "step_ms=%.3f" % d["ms_per_step"], "k2_ms=%.3f" % r["filter_ms_per_launch"], "Tcmp/s=%.2f" % r["achieved"], "frac=%.2f" % r["frac"], "popc_frac=%.2f" % r["popc_equiv_frac"], "e2e=%.3g" % d["e2e"]["value"], "matches=%d" % d["matches_per_step"], "cand=%d" % d["verifier_candidates_per_step"])
+  d=json.loads(sys.stdin.read()); r=d["roofline"]; v=d.get("verify") or {}
+  print(d["config"]["cell"], "step_ms=%.3f" % d["ms_per_step"], "k2_ms=%.3f" % r["filter_ms_per_launch"], "k3_ms=%.3f" % v.get("ms_per_step", 0), "Tcmp/s=%.2f" % r["achieved"], "frac=%.2f" % r["frac"], "popc_frac=%.2f" % r["popc_equiv_frac"], "e2e=%.3g" % d["e2e"]["value"], "matches=%d" % d["matches_per_step"], "cand=%d" % d["verifier_candidates_per_step"])
 except Exception as e: print("parse error", e)')"
   done
 done
