@@ -544,7 +544,17 @@ __global__ void __launch_bounds__(kBigThreads) k_seg_sort_big(const uint64_t* __
         __syncthreads();
         lo = s_lo;
         const uint64_t span = (uint64_t)s_hi - lo + 1;
-        auto bucket = [&](uint32_t v) { return (int)(((uint64_t)(v - lo) * (uint64_t)B) / span); };
+        // bucket = floor((v - lo) * B / span) without a 64-bit division per id
+        // (which cost more than the rest of the kernel): a multiply by
+        // floor(B * 2^32 / span) and a shift give the quotient or one less,
+        // and one more multiply decides which
+        const uint64_t scale = ((uint64_t)B << 32) / span;
+        auto bucket = [&](uint32_t v) {
+            const uint64_t d = v - lo;
+            uint32_t b = (uint32_t)((d * scale) >> 32);
+            if ((uint64_t)(b + 1u) * span <= d * (uint64_t)B) ++b;
+            return (int)b;
+        };
         for (int i = tid; i < n; i += kBigThreads) atomicAdd(&s_cnt[bucket(seg[i])], 1u);
         __syncthreads();
         // exclusive scan of the bucket counts (one warp)
