@@ -635,6 +635,7 @@ struct ShardBatch {
     std::vector<fpg::Tile> plan;
     std::vector<fpg::SliceTile> splan, splan_x;  // bit-sliced tiles; those of the exact path
     bool plan_valid = false;
+    bool plan_small = false;  // the plan's tiles were made smaller than the full shape (few tiles per CTA)
     std::vector<uint32_t> plan_qcount;  // query length histogram the plan was built for
     fpg_query_options plan_opts{};
     DBuf<unsigned long long> out;
@@ -862,6 +863,7 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
             // first two shrink stages (A/B runs)
             static const uint32_t gpw = (uint32_t)env_double("FPG_TILE_GPW", 2.0);
             static const uint32_t q1 = (uint32_t)env_double("FPG_TILE_Q", 32.0);
+            S.plan_small = count_tiles() < target;
             while (count_tiles() < target && (qchunk > 16 || per > grp)) {
                 if (per > gpw * w8) per >>= 1;                 // down to gpw groups per warp
                 else if (qchunk > q1) qchunk >>= 1;            // then q1 queries
@@ -1128,6 +1130,12 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
                 return pl.size() > r ? (uint32_t)((pl.size() - r + R - 1) / R) : 0u;
             };
             SP.tile_stride = R;
+            // barrier-free tiles for plans whose tiles were shrunk (small batches)
+            SP.no_barrier = S.plan_small ? 1 : 0;
+            {
+                const double nb_env = env_double("FPG_NO_BARRIER", -1.0);  // A/B and tests: 0 / 1 forces it
+                if (nb_env >= 0) SP.no_barrier = nb_env != 0.0;
+            }
             for (uint32_t r = 0; r < R; ++r) {
                 if (r) {  // the rounds reuse the tile counters and the record buffer
                     CK(cudaMemsetAsync(S.counters.p + 2, 0, sizeof(unsigned long long), st));

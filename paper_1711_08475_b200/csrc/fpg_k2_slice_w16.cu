@@ -10,21 +10,31 @@ namespace {
 template <int NP, int FW, int EXTRA, int S, bool X = false>
 void launch_slice(const fpg::SliceTile* tiles, uint32_t ntiles, const fpg::SliceParams& P, cudaStream_t st,
                   int device) {
-    // the common options (filter + stats + window on, k = 1) run the HOT instantiation
+    // the common options (filter + stats + window on, k = 1) run the HOT
+    // instantiation; small batches (P.no_barrier) the barrier-free one when
+    // its double-buffered query data fits
     const bool hot = P.use_fp && P.stats && P.wskip && !P.exhaustive && P.k == 1;
-    auto kern = hot ? fpg::k_slice<NP, FW, EXTRA, S, true, X> : fpg::k_slice<NP, FW, EXTRA, S, false, X>;
-    constexpr size_t smem = fpg::slice_smem_bytes(NP + S);
-    static int resident[2][64] = {{0}};  // per variant and device: CTAs resident on the whole GPU (0 = not queried)
+    constexpr bool kCanNB = fpg::slice_no_barrier(NP + S);
+    const bool nb = kCanNB && P.no_barrier;
+    using Kern = void (*)(const fpg::SliceTile*, uint32_t, const fpg::SliceParams);
+    Kern kern;
+    if constexpr (kCanNB)
+        kern = nb ? (hot ? fpg::k_slice<NP, FW, EXTRA, S, true, X, true> : fpg::k_slice<NP, FW, EXTRA, S, false, X, true>)
+                  : (hot ? fpg::k_slice<NP, FW, EXTRA, S, true, X, false> : fpg::k_slice<NP, FW, EXTRA, S, false, X, false>);
+    else
+        kern = hot ? fpg::k_slice<NP, FW, EXTRA, S, true, X, false> : fpg::k_slice<NP, FW, EXTRA, S, false, X, false>;
+    const size_t smem = fpg::slice_smem_bytes(NP + S, nb);
+    static int resident[2][2][64] = {{{0}}};  // per variant and device: CTAs resident on the whole GPU (0 = not queried)
     (void)X;
     const int dv = device & 63;
-    if (!resident[hot][dv]) {
+    if (!resident[hot][nb][dv]) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int sms = 148, per_sm = 0;
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, fpg::kSliceThreads, smem));
-        resident[hot][dv] = sms * std::max(per_sm, 1);
+        resident[hot][nb][dv] = sms * std::max(per_sm, 1);
     }
-    const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)resident[hot][dv]);
+    const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)resident[hot][nb][dv]);
     kern<<<(unsigned)std::max<uint64_t>(grid, 1), fpg::kSliceThreads, smem, st>>>(tiles, ntiles, P);
     CK(cudaGetLastError());
 }

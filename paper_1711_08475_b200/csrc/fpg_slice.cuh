@@ -133,6 +133,7 @@ struct SliceParams {
     // the launch scans tiles tile_off + i * tile_stride, i < ntiles (round r of
     // R takes every R-th tile, so every round sees the plan's mix of lengths)
     uint32_t tile_off, tile_stride;
+    int32_t no_barrier;         // tiles without CTA barriers (kernels whose double-buffered query data fits)
 };
 
 __device__ __forceinline__ int stride_of_len(int len) { return len <= 16 ? 16 : (len + 15) & ~15; }
@@ -186,9 +187,22 @@ struct SliceShape {
     static_assert(NPT % 2 == 0, "plane pairs");
 };
 
+// Tiles without CTA barriers (below): the tile's query data is double
+// buffered, which fits two CTAs per SM while the masks are small enough.
+__host__ __device__ constexpr bool slice_no_barrier(int npt) { return npt <= 40; }
 // Dynamic shared memory of k_slice<NP, .., S>.
-__host__ __device__ constexpr size_t slice_smem_bytes(int npt) {
-    return (size_t)kSliceQ * npt * 8 + 12u * kSliceQ + 8u * kSliceCap * kSliceThreads + 2u * kSliceQ * kSliceWarps;
+__host__ __device__ constexpr size_t slice_smem_bytes(int npt, bool nb) {
+    return ((size_t)kSliceQ * npt * 8 + 12u * kSliceQ) * (nb ? 2 : 1) + 8u * kSliceCap * kSliceThreads +
+           2u * kSliceQ * kSliceWarps;
+}
+// Flags between the warps of a CTA (shared memory, CTA scope).
+__device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v) : "memory");
 }
 
 // HOT: the options of the common run fixed at compile time (fingerprint
@@ -202,7 +216,7 @@ __host__ __device__ constexpr size_t slice_smem_bytes(int npt) {
 // counters count the positions whose codes differ, and a word is a candidate
 // iff at most k positions differ: exactly hamming_bounded's test
 // (edit_distance.hpp:18-27), so the verifier sees only true matches.
-template <int NP, int FW, int EXTRA, int S, bool HOT, bool X = false>
+template <int NP, int FW, int EXTRA, int S, bool HOT, bool X = false, bool NB = false>
 __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __restrict__ tiles, uint32_t ntiles,
                                                             const __grid_constant__ SliceParams P) {
     using Sh = SliceShape<NP, FW, EXTRA, S>;
@@ -212,48 +226,125 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
     const bool o_wskip = HOT || P.wskip;
     const bool o_exhaustive = !HOT && P.exhaustive;
     const int o_k = HOT ? 1 : P.k;
+    // NB: no CTA barrier per tile.  The tile's query data (masks, ids, byte
+    // offsets, lengths, weights, survivor counts, group counter) lives in two
+    // buffers used by alternate tiles.  The first warp to run out of groups in
+    // tile n claims the set-up of tile n + 1 (a CAS on s_claim), waits until
+    // every warp has left tile n - 1 (the buffer's previous user; its last
+    // leaver also posts the tile's per-query survivor counts), fills the
+    // buffer alone and publishes it; the other warps move on to tile n + 1
+    // as they finish, so nobody waits for the tile's slowest slab group.
+    // The host picks it per launch (P.no_barrier): small batches, whose tiles
+    // hold a few slab groups per warp, lose up to 15% of K2 to the barrier;
+    // full-size tiles (config 5) run 0-4% faster with it, since the barrier
+    // variant loads each warp's first group during the set-up.
+    // Two instantiations: the launcher takes NB when P.no_barrier is set and
+    // the double buffers fit (a run-time switch inside one kernel cost the
+    // full-size tiles 3-7%).
+    static_assert(!NB || slice_no_barrier(NPT), "double-buffered query data must fit");
+    constexpr int NBUF = NB ? 2 : 1;
+    constexpr uint32_t kEndTile = 0xffffffffu;
     extern __shared__ __align__(16) uint8_t smem[];
-    uint2* s_qm = reinterpret_cast<uint2*>(smem);                           // [kSliceQ][NPT] (s, m)
-    uint32_t* s_qid = reinterpret_cast<uint32_t*>(s_qm + kSliceQ * NPT);    // [kSliceQ]: input query id
-    uint32_t* s_qoff = s_qid + kSliceQ;                                     // [kSliceQ]: byte offset / 16 in the query blob
-    uint32_t* s_qlen = s_qoff + kSliceQ;                                    // [kSliceQ]: length
-    uint2* s_queue = reinterpret_cast<uint2*>(s_qlen + kSliceQ);            // [cap][threads]
+    uint2* s_qm_all = reinterpret_cast<uint2*>(smem);                                     // [NBUF][kSliceQ][NPT] (s, m)
+    uint32_t* s_qid_all = reinterpret_cast<uint32_t*>(s_qm_all + NBUF * kSliceQ * NPT);   // [NBUF][kSliceQ]: input query id
+    uint32_t* s_qoff_all = s_qid_all + NBUF * kSliceQ;                                    // [NBUF][kSliceQ]: byte offset / 16 in the query blob
+    uint32_t* s_qlen_all = s_qoff_all + NBUF * kSliceQ;                                   // [NBUF][kSliceQ]: length
+    uint2* s_queue = reinterpret_cast<uint2*>(s_qlen_all + NBUF * kSliceQ);               // [cap][threads]
     uint16_t* s_qlist = reinterpret_cast<uint16_t*>(s_queue + kSliceCap * kSliceThreads);  // [warps][kSliceQ]
-    __shared__ uint32_t s_grp;  // next slab group of the tile
-    __shared__ uint32_t s_next[2];  // next tile index, double-buffered by iteration parity
-    __shared__ uint32_t s_surv[kSliceQ];
-    __shared__ uint32_t s_qw[2][kSliceQ];  // query group weights: even, odd nibbles (byte vectors)
+    __shared__ uint32_t s_grp_all[NBUF];  // next slab group of the tile
+    __shared__ uint32_t s_next[2];  // next tile index, double-buffered by iteration parity (barrier variant)
+    __shared__ uint32_t s_surv_all[NBUF][kSliceQ];
+    __shared__ uint32_t s_qw_all[NBUF][2][kSliceQ];  // query group weights: even, odd nibbles (byte vectors)
+    // NB flags, per buffer: the tile it holds, completed set-ups, retired
+    // uses, warps that have left the current use; s_claim: next tile
+    // iteration whose set-up nobody has claimed
+    __shared__ uint32_t s_tile[2], s_ready[2], s_retired[2], s_done[2], s_claim;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     unsigned long long surv_warp = 0;  // lanes 0, 1: the warp's fingerprint survivors
     unsigned long long scanned_warp = 0;  // lane 0
 
-    if (tid == 0) s_next[0] = atomicAdd(P.tile_counter, 1u);
-    __syncthreads();
-    uint32_t t = s_next[0];
-    for (uint32_t it = 1; t < ntiles; ++it) {
-        const SliceTile tl = tiles[(uint64_t)t * P.tile_stride + P.tile_off];
-        if (tid == 0) s_next[it & 1] = atomicAdd(P.tile_counter, 1u);  // read after the end-of-tile barrier
-
-        // query (s, m) masks, ids and group weights; one query per thread
-        for (uint32_t j = tid; j < tl.q_count; j += kSliceThreads) {
-            const uint32_t qp = tl.q_begin + j;
+    // query (s, m) masks, ids, byte offsets and group weights of a tile into
+    // buffer p; query j0, j0 + jstep, ... by the calling thread
+    auto setup = [&](int p, const SliceTile& tq, uint32_t j0, uint32_t jstep) {
+        uint2* qm_p = s_qm_all + p * kSliceQ * NPT;
+        for (uint32_t j = j0; j < tq.q_count; j += jstep) {
+            const uint32_t qp = tq.q_begin + j;
             const uint64_t f = __ldg(P.q_fp + qp);
             const uint32_t g = __ldg(P.q_sigp + qp);
             const uint32_t id = P.q_ids[qp];
-            uint2* dst = s_qm + j * NPT;
+            uint2* dst = qm_p + j * NPT;
 #pragma unroll
             for (int b = 0; b < NPT; ++b) {
                 const uint32_t bit = b < NP ? (uint32_t)(f >> b) & 1u : (g >> (b - NP)) & 1u;
                 dst[b] = bit ? make_uint2(0xffffffffu, 0xffffffffu) : make_uint2(1u, 0u);
             }
-            s_qid[j] = id;
+            s_qid_all[p * kSliceQ + j] = id;
             const int m = P.q_len[qp];
-            s_qlen[j] = (uint32_t)m;
-            s_qoff[j] = (uint32_t)((P.q_bbase[m] + (uint64_t)(qp - P.q_start[m]) * stride_of_len(m)) >> 4);
-            s_surv[j] = 0u;
+            s_qlen_all[p * kSliceQ + j] = (uint32_t)m;
+            s_qoff_all[p * kSliceQ + j] = (uint32_t)((P.q_bbase[m] + (uint64_t)(qp - P.q_start[m]) * stride_of_len(m)) >> 4);
+            s_surv_all[p][j] = 0u;
             const uint32_t qw = o_wskip ? P.q_weight[qp] : 0u;
-            s_qw[0][j] = qw & kNib;
-            s_qw[1][j] = (qw >> 4) & kNib;
+            s_qw_all[p][0][j] = qw & kNib;
+            s_qw_all[p][1][j] = (qw >> 4) & kNib;
+        }
+    };
+    // NB: one warp claims the next tile and sets up iteration n in buffer n & 1
+    auto setup_next = [&](uint32_t n) {
+        const int p = (int)(n & 1u);
+        if (lane == 0)
+            while (ld_acquire_cta(&s_retired[p]) != (n >> 1)) __nanosleep(32);
+        __syncwarp();
+        uint32_t tn = 0;
+        if (lane == 0) tn = atomicAdd(P.tile_counter, 1u);
+        tn = __shfl_sync(0xffffffffu, tn, 0);
+        if (tn < ntiles) {
+            const SliceTile tq = tiles[(uint64_t)tn * P.tile_stride + P.tile_off];
+            setup(p, tq, (uint32_t)lane, 32u);
+        }
+        if (lane == 0) {
+            s_tile[p] = tn < ntiles ? tn : kEndTile;
+            s_grp_all[p] = 0u;
+        }
+        __threadfence_block();
+        __syncwarp();
+        if (lane == 0) st_release_cta(&s_ready[p], (n >> 1) + 1u);
+    };
+
+    uint32_t t = 0;
+    if constexpr (NB) {
+        if (tid == 0) {
+            s_ready[0] = s_ready[1] = s_retired[0] = s_retired[1] = s_done[0] = s_done[1] = 0u;
+            s_claim = 1u;  // iteration 0 is set up by warp 0 right here
+        }
+        __syncthreads();
+        if (warp == 0) setup_next(0u);
+    } else {
+        if (tid == 0) s_next[0] = atomicAdd(P.tile_counter, 1u);
+        __syncthreads();
+        t = s_next[0];
+    }
+    for (uint32_t it = NB ? 0u : 1u;; ++it) {
+        const int pb = NB ? (int)(it & 1u) : 0;  // this tile's buffer
+        if constexpr (NB) {
+            if (lane == 0)
+                while (ld_acquire_cta(&s_ready[pb]) != (it >> 1) + 1u) __nanosleep(32);
+            __syncwarp();
+            t = s_tile[pb];
+            if (t == kEndTile) break;
+        } else {
+            if (t >= ntiles) break;
+        }
+        const SliceTile tl = tiles[(uint64_t)t * P.tile_stride + P.tile_off];
+        uint2* const s_qm = s_qm_all + pb * kSliceQ * NPT;
+        uint32_t* const s_qid = s_qid_all + pb * kSliceQ;
+        uint32_t* const s_qoff = s_qoff_all + pb * kSliceQ;
+        uint32_t* const s_qlen = s_qlen_all + pb * kSliceQ;
+        uint32_t* const s_surv = s_surv_all[pb];
+        uint32_t(*const s_qw)[kSliceQ] = s_qw_all[pb];
+        uint32_t* const s_grp = &s_grp_all[pb];
+        if constexpr (!NB) {
+            if (tid == 0) s_next[it & 1] = atomicAdd(P.tile_counter, 1u);  // read after the end-of-tile barrier
+            setup(0, tl, (uint32_t)tid, (uint32_t)kSliceThreads);  // one query per thread
         }
         // this lane's slabs of slab group g (SL rows of 32 slabs), the
         // group's valid words and its group-weight box
@@ -286,12 +377,15 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
             // the group's weight box, precomputed at construction (k_group_box)
             box = o_wskip ? __ldg(P.gbox + tl.gbox_base + g) : make_uint2(wlo, whi);
         };
-        // warp w's first group is group w: its planes load while the queries
-        // are set up; later groups are claimed from s_grp
+        // barrier variant: warp w's first group is group w, its planes load
+        // while the queries are set up; later groups (NB: all groups) are
+        // claimed from s_grp
         uint32_t g = (uint32_t)warp;
-        if (g < n_grp) load_group(g);
-        if (tid == 0) s_grp = (uint32_t)kSliceWarps;
-        __syncthreads();
+        if constexpr (!NB) {
+            if (g < n_grp) load_group(g);
+            if (tid == 0) *s_grp = (uint32_t)kSliceWarps;
+            __syncthreads();
+        }
 
         // The lane's queue is addressed by a running shared-memory pointer
         // (32-bit window address): a push is one store and one add.
@@ -514,9 +608,9 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
         {
             const uint32_t span = 2u * (uint32_t)o_k;
             uint16_t* ql = s_qlist + warp * kSliceQ;
-            for (bool first = true;; first = false) {
+            for (bool first = !NB;; first = false) {
                 if (!first) {
-                    if (lane == 0) g = atomicAdd(&s_grp, 1u);
+                    if (lane == 0) g = atomicAdd(s_grp, 1u);
                     g = __shfl_sync(0xffffffffu, g, 0);
                     if (g < n_grp) load_group(g);
                 }
@@ -549,11 +643,35 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
             }
         }
         if (verify) flush();
-        __syncthreads();  // tile consumed; s_next[it & 1] and s_surv complete
-        if (o_stats)
-            for (uint32_t j = tid; j < tl.q_count; j += kSliceThreads)
-                if (s_surv[j]) atomicAdd(&P.q_survivors[s_qid[j]], s_surv[j]);
-        t = s_next[it & 1];
+        if constexpr (NB) {
+            // leave the tile: the last warp out posts the survivor counts and
+            // retires the buffer; the first one out sets up the next tile
+            __threadfence_block();
+            __syncwarp();
+            uint32_t left = 0;
+            if (lane == 0) left = atomicAdd(&s_done[pb], 1u);
+            left = __shfl_sync(0xffffffffu, left, 0);
+            if (left == (uint32_t)kSliceWarps - 1u) {
+                __threadfence_block();
+                if (o_stats)
+                    for (uint32_t j = (uint32_t)lane; j < tl.q_count; j += 32u)
+                        if (s_surv[j]) atomicAdd(&P.q_survivors[s_qid[j]], s_surv[j]);
+                __syncwarp();
+                if (lane == 0) {
+                    s_done[pb] = 0u;
+                    st_release_cta(&s_retired[pb], (it >> 1) + 1u);
+                }
+            }
+            uint32_t won = 0;
+            if (lane == 0) won = atomicCAS(&s_claim, it + 1u, it + 2u) == it + 1u;
+            if (__shfl_sync(0xffffffffu, won, 0)) setup_next(it + 1u);
+        } else {
+            __syncthreads();  // tile consumed; s_next[it & 1] and s_surv complete
+            if (o_stats)
+                for (uint32_t j = tid; j < tl.q_count; j += kSliceThreads)
+                    if (s_surv[j]) atomicAdd(&P.q_survivors[s_qid[j]], s_surv[j]);
+            t = s_next[it & 1];
+        }
     }
     if (o_stats && lane < 2 && surv_warp) atomicAdd(P.survivors_total, surv_warp);
     if (lane == 0 && scanned_warp) atomicAdd(P.scanned, scanned_warp);

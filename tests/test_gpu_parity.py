@@ -296,6 +296,23 @@ def test_candidate_buffer_rounds(oracle, monkeypatch, limit):
         b.close()
 
 
+@pytest.mark.parametrize("no_barrier", ["0", "1"])
+def test_tiles_with_and_without_barriers(oracle, monkeypatch, no_barrier):
+    """K2 runs a tile's warps either between two CTA barriers or, for small
+    batches, without barriers (double-buffered query data, the first warp out
+    sets up the next tile).  Both variants forced on the same inputs,
+    including tiles with fewer slab groups than warps and many tiles per CTA."""
+    monkeypatch.setenv("FPG_NO_BARRIER", no_barrier)
+    for cfg, n, nq in [(2, 120_000, 900), (3, 150_000, 700), (5, 300_000, 3000)]:
+        blob, offs = generate_dictionary(cfg, n=n)
+        qblob, qoffs = generate_queries(cfg, blob, offs, nq=nq)
+        for variant, width, metric in [(Variant.Occurrence, 16, Metric.Hamming), (Variant.Count, 16, Metric.Levenshtein)]:
+            s = make_scheme(blob, variant, width)
+            with GpuFingerprintedDictionary((blob, offs), s) as d:
+                csr, st = d.query_batch((qblob, qoffs), QueryOptions(metric, 1, True, True), True)
+            assert_same(csr, st, *oracle.query_batch(blob, offs, qblob, qoffs, osch(s), metric, 1, True, True))
+
+
 def test_k4_segment_size_classes(oracle, exact_path):
     """K4 sorts each query's matches by word id in one of three ways: <= 32
     (warp bitonic), 33..4096 (one CTA, shared-memory bitonic) and larger

@@ -105,7 +105,9 @@ def traffic(path, key, out_json):
     tot = sum(float(d[k].replace(",", "")) * scale.get(u[k], 1) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     db = json.load(open(out_json)) if os.path.exists(out_json) else {}
     db[key] = {"kernel": d.get("Kernel Name", "?"), "dram_bytes": tot, "report": os.path.basename(path),
-               "duration_us": float(d["gpu__time_duration.sum"].replace(",", "")) * (1e-3 if u["gpu__time_duration.sum"] == "nsecond" else 1.0)}
+               "duration_us": float(d["gpu__time_duration.sum"].replace(",", "")) *
+               {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6}.get(
+                   u["gpu__time_duration.sum"], 1.0)}
     json.dump(db, open(out_json, "w"), indent=1, sort_keys=True)
     print(key, db[key])
 
