@@ -571,6 +571,8 @@ def main():
                   "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm, "peak_basis": hbm_basis,
                   "traffic": profiled_traffic(f"config{args.config}", w.cell_name() + " k_verify"),
                   "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",
+                  "note": "the warps claim the records in stream order, so the candidate words hit L2 and the "
+                          "DRAM traffic is essentially the records; ncu shows the kernel issue-bound (DESIGN.md section 3)",
                   "candidate_records": t0s.get("candidate_records", 0), "rounds": t0s.get("verify_rounds", 1),
                   "bytes_basis": f"16 B per record (upper bound: records of the largest round x rounds) + {w_stride} B "
                                  "per candidate word (random 32-byte sectors in practice) + 8 B per match key"}
