@@ -93,8 +93,11 @@ def ops_per_comparison(scheme, sig_fields: int, exact: bool = False) -> float:
         return 6 * q4 + (q4 + 1) // 2 + 4 * ((n % 4 + 1) // 2)
 
     ors = nf * (0 if fw == 1 else 1 if fw <= 3 else 2)
-    if exact:  # position fields: a 5-plane OR (2 LOP3) each, then their own counter
-        return (ors + csa(nf + extra) + 2 * X_LEN + csa(X_LEN) + 1) / 32.0
+    if exact:
+        # position fields: a 5-plane OR (2 LOP3) each, their own counter and the
+        # pass mask (the scheme fields are not counted there any more: QueryStats
+        # come from the fingerprint histograms)
+        return (2 * X_LEN + csa(X_LEN) + 1) / 32.0
     return (ors + csa(nf + extra) + csa(sig_fields) + 1) / 32.0
 
 

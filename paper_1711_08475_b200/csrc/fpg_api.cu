@@ -295,6 +295,14 @@ struct Collection {
     DBuf<uint64_t> wkey_a, wkey_b;  // scratch: (length << 32 | group weights) sort keys
     DBuf<uint32_t> d_slab_start, d_count;
     DBuf<uint64_t> d_plane_base;
+    // W = 16 dictionaries: fingerprint histogram per present length (+ one over
+    // all lengths) and the XOR masks within F_D <= 2 (k_fp_stats): QueryStats
+    // without survivor counters in K2
+    DBuf<uint32_t> fph;        // [(nh + 1) * 65536]
+    DBuf<int32_t> d_hslot;     // per length: histogram slot or -1
+    DBuf<uint32_t> d_hfirst;   // per slot: first sorted position
+    DBuf<uint16_t> d_hdelta;   // 0 first
+    int nh = 0, n_hdelta = 0;
     // scratch (len_b = lengths in sorted order; kept for query collections)
     DBuf<uint16_t> len_a, len_b;
     DBuf<uint32_t> idx_a, idx_b;
@@ -538,8 +546,56 @@ struct Collection {
                     ++launches;
                 }
             }
+            launches += build_fp_hist(P, st);
         }
         return launches;
+    }
+
+    // Fingerprint histograms for QueryStats (fpg_kernels.cuh, k_fp_stats): 16-bit
+    // schemes with at most kMaxHistLengths present lengths.
+    static constexpr int kMaxHistLengths = 256;
+    uint64_t build_fp_hist(const fpg::SchemeParams& P, cudaStream_t st) {
+        nh = 0;
+        if (P.width != 16 || !n) return 0;
+        const int L1 = fpg::kMaxLen + 1;
+        std::vector<int32_t> hslot(L1, -1);
+        std::vector<uint32_t> hfirst;
+        for (int L = 0; L < L1; ++L)
+            if (count[L]) {
+                hslot[L] = (int32_t)hfirst.size();
+                hfirst.push_back(start[L]);
+            }
+        if ((int)hfirst.size() > kMaxHistLengths) return 0;
+        nh = (int)hfirst.size();
+        // XOR masks touching at most two fields (F_D <= 2), 0 first
+        std::vector<uint16_t> fmask;  // one bit mask per field
+        const int fw = P.variant == FPG_COUNT ? P.b : P.variant == FPG_POSITION ? P.p : 1;
+        const int extra = P.variant == FPG_POSITION ? P.extra : 0;
+        const int nf = (16 - extra) / fw;
+        for (int f = 0; f < nf; ++f) fmask.push_back((uint16_t)(((1u << fw) - 1u) << (16 - fw * (f + 1))));
+        for (int e = 0; e < extra; ++e) fmask.push_back((uint16_t)(1u << e));
+        std::vector<uint16_t> deltas{0};
+        auto values = [&](uint16_t m, auto&& f) {  // every non-zero value inside mask m
+            for (uint32_t v = m; v; v = (v - 1) & m) f((uint16_t)v);
+        };
+        for (size_t a = 0; a < fmask.size(); ++a)
+            values(fmask[a], [&](uint16_t va) {
+                deltas.push_back(va);
+                for (size_t b = a + 1; b < fmask.size(); ++b) values(fmask[b], [&](uint16_t vb) { deltas.push_back(va | vb); });
+            });
+        n_hdelta = (int)deltas.size();
+        fph.reserve((size_t)(nh + 1) * 65536);
+        d_hslot.reserve(L1);
+        d_hfirst.reserve(nh);
+        d_hdelta.reserve(deltas.size());
+        CK(cudaMemsetAsync(fph.p, 0, (size_t)(nh + 1) * 65536 * sizeof(uint32_t), st));
+        CK(cudaMemcpyAsync(d_hslot.p, hslot.data(), L1 * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d_hfirst.p, hfirst.data(), nh * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d_hdelta.p, deltas.data(), deltas.size() * sizeof(uint16_t), cudaMemcpyHostToDevice, st));
+        fpg::k_fp_hist<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(fp.p, n, d_hfirst.p, nh, fph.p);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(st));  // the host vectors above go out of scope
+        return 1;
     }
 
     void drop_scratch() {
@@ -803,7 +859,13 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
                                          kNumCounters);
     const Collection& Q = S.queries;
     const Collection& W = sh.dict;
-    const bool count_only_pass = o.want_stats && o.use_filter && o.metric == FPG_LEVENSHTEIN && !o.length_prefilter;
+    // QueryStats::verified from the fingerprint histograms instead of K2's
+    // survivor counters (W = 16 dictionaries, k <= 1; FPG_HIST_STATS=0: A/B)
+    static const bool hist_on = env_double("FPG_HIST_STATS", 1.0) != 0.0;
+    const bool ext_stats = hist_on && D->slice && o.k <= 1 && W.nh > 0 && o.want_stats && o.use_filter && !o.exhaustive &&
+                           supports(D->scheme.variant, o.metric);
+    const bool count_only_pass =
+        !ext_stats && o.want_stats && o.use_filter && o.metric == FPG_LEVENSHTEIN && !o.length_prefilter;
     uint64_t executed = 0;
     std::vector<fpg::Tile>& plan = S.plan;
     std::vector<fpg::SliceTile>& splan = S.splan;
@@ -1017,7 +1079,7 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
         SP.survivors_total = S.counters.p + 1;
         SP.tile_counter = reinterpret_cast<unsigned int*>(S.counters.p + 2);
         SP.k = o.k;
-        SP.stats = (o.want_stats && o.use_filter) ? 1 : 0;
+        SP.stats = (o.want_stats && o.use_filter && !ext_stats) ? 1 : 0;
         SP.use_fp = supports(D->scheme.variant, o.metric) && !o.exhaustive ? 1 : 0;
         SP.exhaustive = o.exhaustive ? 1 : 0;
         SP.wskip = SP.use_fp && !o.exhaustive && !g_no_wskip ? 1 : 0;
@@ -1194,6 +1256,17 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
             ++S.launches;
         }
         CK(cudaEventRecord(S.ev[2], st));
+        if (ext_stats && nq) {
+            // per-query fingerprint survivors from the histograms (k = 0: the
+            // query's own fingerprint only, the first mask)
+            const int span = o.metric == FPG_HAMMING ? 0 : o.k;
+            const int all_len = (o.metric == FPG_LEVENSHTEIN && !o.length_prefilter) ? 1 : 0;
+            fpg::k_fp_stats<<<(unsigned)std::min<uint64_t>(cdiv(nq, 8), 148 * 16), 256, 0, st>>>(
+                Q.fp.p, Q.len_b.p, Q.ids.p, nq, W.fph.p, W.d_hslot.p, W.nh, W.max_len, W.d_hdelta.p,
+                o.k == 0 ? 1 : W.n_hdelta, span, all_len, S.qsurv.p, S.counters.p + 1);
+            CK(cudaGetLastError());
+            ++S.launches;
+        }
         // K4: offsets = exclusive scan of the per-query match counts, keys
         // scattered into their query's segment, then each segment of <=
         // kSegMax matches sorted by one warp; larger ones are listed.

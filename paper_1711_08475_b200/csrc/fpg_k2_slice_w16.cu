@@ -13,7 +13,8 @@ void launch_slice(const fpg::SliceTile* tiles, uint32_t ntiles, const fpg::Slice
     // the common options (filter + stats + window on, k = 1) run the HOT
     // instantiation; small batches (P.no_barrier) the barrier-free one when
     // its double-buffered query data fits
-    const bool hot = P.use_fp && P.stats && P.wskip && !P.exhaustive && P.k == 1;
+    // (W = 16: HOT has no survivor counters, the histograms give the stats)
+    const bool hot = P.use_fp && (NP == 16 ? !P.stats : P.stats != 0) && P.wskip && !P.exhaustive && P.k == 1;
     constexpr bool kCanNB = fpg::slice_no_barrier(NP + S);
     const bool nb = kCanNB && P.no_barrier;
     using Kern = void (*)(const fpg::SliceTile*, uint32_t, const fpg::SliceParams);

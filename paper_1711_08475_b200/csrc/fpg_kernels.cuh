@@ -609,6 +609,77 @@ __global__ void __launch_bounds__(kBigThreads) k_seg_sort_big(const uint64_t* __
 }
 #endif
 
+// ---------------------------------------------------------------- QueryStats by fingerprint histogram
+// W = 16 dictionaries: QueryStats::verified (dictionary.hpp:102-110: the
+// words that pass the length test and the fingerprint test F_D <= 2k) does not
+// need the pair scan.  F_D counts the fields whose bits differ
+// (ComparisonTables, fingerprint.hpp:171-214), so the fingerprints within
+// F_D <= 2k of a query's are fp ^ d for the XOR masks d that touch at most 2k
+// fields (137 masks for 16 one-bit fields at k = 1, 277 for count-16 b = 2,
+// 562 for position-16 p = 3; the host lists them, 0 first), and
+//     verified(q) = sum over compatible lengths L, masks d of H_L[fp(q) ^ d]
+// with H_L the histogram of the fingerprints of the words of length L.  K2
+// then runs without its survivor counters.
+//
+// k_fp_hist: H[slot(L)][fp] over the sorted dictionary (slot nh = all lengths).
+#ifndef FPG_K2_TU  // defined once, in fpg_api.cu
+__global__ void k_fp_hist(const uint64_t* __restrict__ fp, uint64_t n, const uint32_t* __restrict__ slot_first,
+                          int nh, uint32_t* __restrict__ hist) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int lo = 0, hi = nh;  // largest slot with slot_first[slot] <= i
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (slot_first[mid] <= i) lo = mid;
+        else hi = mid;
+    }
+    const uint32_t f = (uint32_t)fp[i] & 0xffffu;
+    atomicAdd(&hist[(uint64_t)lo * 65536u + f], 1u);
+    atomicAdd(&hist[(uint64_t)nh * 65536u + f], 1u);
+}
+
+// One warp per (sorted) query.  span: compatible lengths are m - span .. m +
+// span; all_lengths: every word is length-compatible (Levenshtein without the
+// length prefilter, dictionary.hpp:94-101).
+__global__ void __launch_bounds__(256) k_fp_stats(const uint64_t* __restrict__ q_fp, const uint16_t* __restrict__ q_len,
+                                                  const uint32_t* __restrict__ q_ids, uint64_t nq,
+                                                  const uint32_t* __restrict__ hist, const int32_t* __restrict__ hslot,
+                                                  int nh, int max_len, const uint16_t* __restrict__ deltas, int nd,
+                                                  int span, int all_lengths, uint32_t* __restrict__ q_survivors,
+                                                  unsigned long long* __restrict__ survivors_total) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long warp_sum = 0;
+    for (uint64_t q = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nq; q += warps) {
+        const uint32_t f = (uint32_t)q_fp[q] & 0xffffu;
+        const int m = (int)q_len[q];
+        const uint32_t* h[3] = {nullptr, nullptr, nullptr};
+        if (all_lengths) {
+            h[0] = hist + (uint64_t)nh * 65536u;
+        } else {
+            for (int t = 0; t <= 2 * span; ++t) {
+                const int L = m - span + t;
+                const int sl = (L >= 0 && L <= max_len) ? hslot[L] : -1;
+                if (sl >= 0) h[t] = hist + (uint64_t)sl * 65536u;
+            }
+        }
+        uint32_t c = 0;
+        for (int i = lane; i < nd; i += 32) {
+            const uint32_t g = f ^ (uint32_t)deltas[i];
+#pragma unroll
+            for (int t = 0; t < 3; ++t)
+                if (h[t]) c += __ldg(h[t] + g);
+        }
+        c = __reduce_add_sync(0xffffffffu, c);
+        if (lane == 0) {
+            q_survivors[q_ids[q]] = c;
+            warp_sum += c;
+        }
+    }
+    if (lane == 0 && warp_sum) atomicAdd(survivors_total, warp_sum);
+}
+#endif
+
 // ---------------------------------------------------------------- CSR merge
 // Shards own ascending, contiguous input-order id ranges, so the global
 // (query asc, word asc) CSR is each query's part rows concatenated in part

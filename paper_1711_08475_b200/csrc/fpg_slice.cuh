@@ -206,9 +206,11 @@ __device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
 }
 
 // HOT: the options of the common run fixed at compile time (fingerprint
-// filter on, QueryStats on, weight window on, k = 1, not exhaustive), so the
-// per-step code carries no uniform branches on them; other runs take the
-// generic instantiation (HOT = false), which reads them from P.
+// filter on, weight window on, k = 1, not exhaustive; survivor counters for
+// QueryStats on for W = 32 / 64 and off for W = 16, whose stats come from the
+// fingerprint histograms, k_fp_stats), so the per-step code carries no
+// uniform branches on them; other runs take the generic instantiation
+// (HOT = false), which reads them from P.
 //
 // X (exact Hamming path, words of <= kXLen bytes): planes NP.. are not sig'
 // but the words' symbol codes, kXBits planes per byte position, and q_sigp
@@ -222,7 +224,9 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
     using Sh = SliceShape<NP, FW, EXTRA, S>;
     constexpr int NPT = Sh::NPT, SL = Sh::SL, NF = Sh::NF;
     const bool o_use_fp = HOT || P.use_fp;
-    const bool o_stats = HOT || P.stats;
+    // HOT kernels of W = 16 dictionaries carry no survivor counters: the host
+    // takes QueryStats::verified from the fingerprint histograms (k_fp_stats)
+    const bool o_stats = HOT ? (NP != 16) : (P.stats != 0);
     const bool o_wskip = HOT || P.wskip;
     const bool o_exhaustive = !HOT && P.exhaustive;
     const int o_k = HOT ? 1 : P.k;
@@ -546,7 +550,8 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
             // scheme fields.  Skipped when they do not bound the metric (halved
             // / position with Levenshtein, filter off): sig' alone stays a
             // valid bound.
-            if (o_use_fp) count(std::integral_constant<int, 0>{}, std::integral_constant<int, NF + EXTRA>{});
+            // (the exact path counts them for QueryStats only)
+            if (o_use_fp && (!X || o_stats)) count(std::integral_constant<int, 0>{}, std::integral_constant<int, NF + EXTRA>{});
             if (o_stats) {  // fingerprint survivors: QueryStats::verified (dictionary.hpp:102-110)
                 uint32_t sv = 0;  // query h in bits [16 h, 16 h + 16): <= 2048 per warp
 #pragma unroll
