@@ -68,7 +68,7 @@ def alu_peak():
         return 64.0, "unmeasured: 16 lanes/clk/SMSP (B300_MICROARCH.md pipe rates)"
 
 
-X_LEN, X_BITS = 4, 5  # the exact Hamming path of short words (fpg_kernels.cuh kXLen / kXBits)
+X_LEN, X_BITS = 6, 5  # the exact Hamming path of short words (fpg_kernels.cuh kXLen / kXBits)
 
 
 def ops_per_comparison(scheme, sig_fields: int, exact: bool = False) -> float:

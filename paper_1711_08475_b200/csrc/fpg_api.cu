@@ -526,7 +526,7 @@ struct Collection {
             if (P.xlen) {
                 // exact path planes (same kernel): fingerprint bits, then the
                 // position codes, for the buckets of words <= kXLen bytes
-                const int xnpt = P.width + fpg::kXBits * fpg::kXLen;
+                const int xnpt = fpg::kXBits * fpg::kXLen;  // code planes only (QueryStats come from the histograms)
                 xplane_base.assign(fpg::kXLen + 1, 0);
                 uint64_t xb = 0;
                 for (int L = 0; L <= fpg::kXLen; ++L) {
@@ -541,7 +541,7 @@ struct Collection {
                                        cudaMemcpyHostToDevice, st));
                     fpg::k_planes<<<(unsigned)cdiv(xsl, fpg::kPlanesSlabs), 32 * fpg::kPlanesSlabs, 0, st>>>(
                         fp.p, xc.p, nullptr, nullptr, d_slab_start.p, d_start.p, d_count.p, d_xplane_base.p,
-                        fpg::kXLen + 1, xsl, P.width, xnpt, xplanes.p);
+                        fpg::kXLen + 1, xsl, 0, xnpt, xplanes.p);
                     CK(cudaGetLastError());
                     ++launches;
                 }
@@ -859,6 +859,10 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
                                          kNumCounters);
     const Collection& Q = S.queries;
     const Collection& W = sh.dict;
+    uint64_t executed = 0;
+    std::vector<fpg::Tile>& plan = S.plan;
+    std::vector<fpg::SliceTile>& splan = S.splan;
+    std::vector<fpg::SliceTile>& splan_x = S.splan_x;
     // QueryStats::verified from the fingerprint histograms instead of K2's
     // survivor counters (W = 16 dictionaries, k <= 1; FPG_HIST_STATS=0: A/B)
     static const bool hist_on = env_double("FPG_HIST_STATS", 1.0) != 0.0;
@@ -866,14 +870,12 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
                            supports(D->scheme.variant, o.metric);
     const bool count_only_pass =
         !ext_stats && o.want_stats && o.use_filter && o.metric == FPG_LEVENSHTEIN && !o.length_prefilter;
-    uint64_t executed = 0;
-    std::vector<fpg::Tile>& plan = S.plan;
-    std::vector<fpg::SliceTile>& splan = S.splan;
-    std::vector<fpg::SliceTile>& splan_x = S.splan_x;
-    // exact Hamming path for the words of <= kXLen bytes (fpg_slice.cuh, X)
+    // exact Hamming path for the words of <= kXLen bytes (fpg_slice.cuh, X);
+    // its kernel holds no scheme planes, so it needs the stats to come from
+    // the histograms (or not to be wanted)
     static const bool exact_on = env_double("FPG_EXACT", 1.0) != 0.0;
     const bool xpath = exact_on && D->params.xlen && o.metric == FPG_HAMMING && o.k <= 1 && !o.exhaustive &&
-                       o.use_filter;
+                       o.use_filter && (ext_stats || !o.want_stats);
     // The tile plan depends only on the batch's length histogram and the
     // options: it is built (and uploaded) once and reused by later runs and
     // by later batches with the same histogram.

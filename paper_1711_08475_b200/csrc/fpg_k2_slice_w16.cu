@@ -14,7 +14,7 @@ void launch_slice(const fpg::SliceTile* tiles, uint32_t ntiles, const fpg::Slice
     // instantiation; small batches (P.no_barrier) the barrier-free one when
     // its double-buffered query data fits
     // (W = 16: HOT has no survivor counters, the histograms give the stats)
-    const bool hot = P.use_fp && (NP == 16 ? !P.stats : P.stats != 0) && P.wskip && !P.exhaustive && P.k == 1;
+    const bool hot = P.use_fp && (NP <= 16 ? !P.stats : P.stats != 0) && P.wskip && !P.exhaustive && P.k == 1;
     constexpr bool kCanNB = fpg::slice_no_barrier(NP + S);
     const bool nb = kCanNB && P.no_barrier;
     using Kern = void (*)(const fpg::SliceTile*, uint32_t, const fpg::SliceParams);
@@ -64,20 +64,17 @@ void dispatch_slice_16(int fw, int nsig, const fpg::SliceTile* tiles, uint32_t n
     }
 }
 
-// The exact Hamming path of short words (k_slice<16, fw, extra, kXBits * kXLen, *, X = true>).
+// The exact Hamming path of short words: k_slice<0, 1, 0, kXBits * kXLen, *, X = true>,
+// code planes only (whatever the scheme's field width).
 void dispatch_slice_16x(int fw, const fpg::SliceTile* tiles, uint32_t ntiles, const fpg::SliceParams& P,
                         cudaStream_t st, int device) {
+    (void)fw;
     constexpr int SX = fpg::kXBits * fpg::kXLen;
     // the exact kernel claims the same slab groups as the sig' kernel (W = 16:
     // NPT <= 32, two slabs per lane): the precomputed group boxes serve both
-    static_assert(fpg::slice_slabs_per_lane(16 + SX) == 2 && fpg::slice_slabs_per_lane(16 + 16) == 2,
+    static_assert(fpg::slice_slabs_per_lane(SX) == 2 && fpg::slice_slabs_per_lane(16 + 16) == 2,
                   "exact path and sig' path must share the slab-group size");
-    switch (fw) {
-        case 1: launch_slice<16, 1, 0, SX, true>(tiles, ntiles, P, st, device); break;
-        case 2: launch_slice<16, 2, 0, SX, true>(tiles, ntiles, P, st, device); break;
-        case 3: launch_slice<16, 3, 16 % 3, SX, true>(tiles, ntiles, P, st, device); break;
-        default: launch_slice<16, 4, 0, SX, true>(tiles, ntiles, P, st, device); break;
-    }
+    launch_slice<0, 1, 0, SX, true>(tiles, ntiles, P, st, device);
 }
 
 }  // namespace fpg_host

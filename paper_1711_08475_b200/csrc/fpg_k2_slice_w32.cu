@@ -15,7 +15,7 @@ void launch_slice(const fpg::SliceTile* tiles, uint32_t ntiles, const fpg::Slice
     // instantiation; small batches (P.no_barrier) the barrier-free one when
     // its double-buffered query data fits
     // (W = 16: HOT has no survivor counters, the histograms give the stats)
-    const bool hot = P.use_fp && (NP == 16 ? !P.stats : P.stats != 0) && P.wskip && !P.exhaustive && P.k == 1;
+    const bool hot = P.use_fp && (NP <= 16 ? !P.stats : P.stats != 0) && P.wskip && !P.exhaustive && P.k == 1;
     constexpr bool kCanNB = fpg::slice_no_barrier(NP + S);
     const bool nb = kCanNB && P.no_barrier;
     using Kern = void (*)(const fpg::SliceTile*, uint32_t, const fpg::SliceParams);

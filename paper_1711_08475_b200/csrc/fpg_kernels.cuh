@@ -25,7 +25,7 @@ namespace fpg {
 constexpr int kMaxLen = 4096;
 // Words of at most kXLen bytes get exact position-code planes (K2's exact
 // Hamming path, fpg_slice.cuh): 5 bits per position.
-constexpr int kXLen = 4;
+constexpr int kXLen = 6;
 constexpr int kXBits = 5;
 
 // Symbol -> slot table and scheme constants.  Passed by value as a kernel

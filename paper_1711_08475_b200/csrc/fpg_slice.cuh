@@ -226,7 +226,8 @@ __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __r
     const bool o_use_fp = HOT || P.use_fp;
     // HOT kernels of W = 16 dictionaries carry no survivor counters: the host
     // takes QueryStats::verified from the fingerprint histograms (k_fp_stats)
-    const bool o_stats = HOT ? (NP != 16) : (P.stats != 0);
+    // (the exact path's kernel has no scheme planes: never any counters)
+    const bool o_stats = X ? false : HOT ? (NP > 16) : (P.stats != 0);
     const bool o_wskip = HOT || P.wskip;
     const bool o_exhaustive = !HOT && P.exhaustive;
     const int o_k = HOT ? 1 : P.k;
