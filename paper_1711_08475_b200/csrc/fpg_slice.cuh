@@ -1,6 +1,6 @@
 // fpg_slice.cuh -- K2 as a bit-sliced scan (sm_100a): no POPC on the pair path.
 //
-// Layout.  The words of one dictionary length bucket, sorted by their four
+// Layout.  The words of one dictionary length bucket, sorted by their eight
 // group weights (input order within equal keys), are cut into slabs of 32
 // consecutive words.  A slab is stored as NPT 32-bit planes:
 // plane b holds bit b of the 32 words' comparison codes (K1b k_planes).
@@ -29,17 +29,18 @@
 // count-16 with 16 sig' fields, against the POPC pipe's 16/clk/SM bound of a
 // per-pair XOR + POPC.
 //
-// Scheduling.  A tile is (<= 128 queries) x (<= 32 slab groups of SL rows of
-// 32 slabs) of one word length.  The CTA writes the tile's query masks to
-// shared memory once; its warps then claim slab groups from a shared counter
-// (warp w's first group prefetched during the setup), load the group's planes
-// into registers, build the group's query list through the weight window and
-// scan it two queries per step.
+// Scheduling.  A tile is (<= 128 queries) x (<= 256 slab groups of SL rows of
+// 32 slabs) of one word length.  The tile's query masks are written to shared
+// memory once; the warps then claim slab groups from a shared counter, load
+// the group's planes into registers, build the group's query list through the
+// weight window and scan it two queries per step.  Full-size tiles run
+// between two CTA barriers (warp w's first group loads during the set-up);
+// small batches take the instantiation without barriers (NB, below).
 //
-// Weight window.  sum_g |gw_g(q) - gw_g(x)| <= F_D over 4 field groups
+// Weight window.  sum_g |gw_g(q) - gw_g(x)| <= F_D over 8 field groups
 // (fp_gweight), so a warp skips the queries whose group weights are more than
-// 2k (L1) away from its slabs' group-weight box: those pairs are rejected by
-// the reference test anyway.
+// 2k (L1) away from its slab group's weight box (k_group_box): those pairs
+// are rejected by the reference test anyway.
 //
 // sig' (internal, exact).  Bytes that are NOT scheme letters are dealt into S
 // extra one-bit occurrence fields (host LUT, frequency round robin).  One edit
@@ -49,7 +50,10 @@
 // Hamming + Levenshtein; halved, position: Hamming).  Counting on through the
 // sig' planes with the same counters therefore never drops a match; it only
 // shrinks the candidate set the byte verifier sees.  QueryStats use the
-// counters as they stand after the scheme planes (the reference's F_D alone).
+// counters as they stand after the scheme planes (the reference's F_D alone)
+// in the W = 32 / 64 kernels; W = 16 dictionaries take them from fingerprint
+// histograms instead (k_fp_stats, fpg_kernels.cuh), and their kernels carry
+// no survivor counters.
 //
 // Candidates (rare) go to a lane-private queue in shared memory as
 // (query, slab row, 32-bit word mask) and leave the kernel as records of the
@@ -212,12 +216,13 @@ __device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
 // uniform branches on them; other runs take the generic instantiation
 // (HOT = false), which reads them from P.
 //
-// X (exact Hamming path, words of <= kXLen bytes): planes NP.. are not sig'
-// but the words' symbol codes, kXBits planes per byte position, and q_sigp
-// holds the queries' codes.  After the scheme fields (QueryStats) fresh
-// counters count the positions whose codes differ, and a word is a candidate
-// iff at most k positions differ: exactly hamming_bounded's test
-// (edit_distance.hpp:18-27), so the verifier sees only true matches.
+// X (exact Hamming path, words of <= kXLen bytes; instantiated with NP = 0):
+// the planes are the words' symbol codes, kXBits planes per byte position,
+// and q_sigp holds the queries' codes.  The counters count the positions
+// whose codes differ, and a word is a candidate iff at most k positions
+// differ: exactly hamming_bounded's test (edit_distance.hpp:18-27), so the
+// verifier sees only true matches.  No scheme planes, no survivor counters:
+// the host takes the path only when QueryStats come from the histograms.
 template <int NP, int FW, int EXTRA, int S, bool HOT, bool X = false, bool NB = false>
 __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __restrict__ tiles, uint32_t ntiles,
                                                             const __grid_constant__ SliceParams P) {
