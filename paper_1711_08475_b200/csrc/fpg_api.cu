@@ -865,7 +865,7 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
     std::vector<fpg::SliceTile>& splan_x = S.splan_x;
     // QueryStats::verified from the fingerprint histograms instead of K2's
     // survivor counters (W = 16 dictionaries, k <= 1; FPG_HIST_STATS=0: A/B)
-    static const bool hist_on = env_double("FPG_HIST_STATS", 1.0) != 0.0;
+    const bool hist_on = env_double("FPG_HIST_STATS", 1.0) != 0.0;  // read per run: tests switch it
     const bool ext_stats = hist_on && D->slice && o.k <= 1 && W.nh > 0 && o.want_stats && o.use_filter && !o.exhaustive &&
                            supports(D->scheme.variant, o.metric);
     const bool count_only_pass =

@@ -313,6 +313,26 @@ def test_tiles_with_and_without_barriers(oracle, monkeypatch, no_barrier):
             assert_same(csr, st, *oracle.query_batch(blob, offs, qblob, qoffs, osch(s), metric, 1, True, True))
 
 
+@pytest.mark.parametrize("hist", ["0", "1"])
+def test_query_stats_from_histograms_or_counters(oracle, monkeypatch, hist):
+    """QueryStats::verified of 16-bit schemes comes from per-length fingerprint
+    histograms (k_fp_stats) or, with FPG_HIST_STATS=0, from K2's survivor
+    counters (generic instantiation, no exact path); both must equal the
+    oracle for every variant, metric, k in {0, 1} and prefilter setting."""
+    monkeypatch.setenv("FPG_HIST_STATS", hist)
+    blob, offs = generate_dictionary(5, n=200_000)
+    qblob, qoffs = generate_queries(5, blob, offs, nq=1500)
+    for variant in (Variant.Occurrence, Variant.OccurrenceHalved, Variant.Count, Variant.Position):
+        s = make_scheme(blob, variant, 16)
+        with GpuFingerprintedDictionary((blob, offs), s) as d:
+            for metric in (Metric.Hamming, Metric.Levenshtein):
+                if not variant_supports(variant, metric):
+                    continue
+                for k, pre in [(1, True), (0, True), (1, False)]:
+                    csr, st = d.query_batch((qblob, qoffs), QueryOptions(metric, k, True, pre), True)
+                    assert_same(csr, st, *oracle.query_batch(blob, offs, qblob, qoffs, osch(s), metric, k, True, pre))
+
+
 def test_k4_segment_size_classes(oracle, exact_path):
     """K4 sorts each query's matches by word id in one of three ways: <= 32
     (warp bitonic), 33..4096 (one CTA, shared-memory bitonic) and larger
