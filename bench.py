@@ -68,6 +68,28 @@ def alu_peak():
         return 64.0, "unmeasured: 16 lanes/clk/SMSP (B300_MICROARCH.md pipe rates)"
 
 
+def imad_peak() -> float:
+    """IMAD thread-ops per clk per SM (FMA pipe), same microbenchmark."""
+    try:
+        return float(json.loads((ROOT / "profiles" / "alu_peak.json").read_text())["imad_per_clk_per_sm"])
+    except (OSError, ValueError, KeyError):
+        return 64.0
+
+
+def imads_per_comparison(scheme, sig_fields: int, exact: bool = False) -> float:
+    """IMAD per comparison (the query XOR of every plane, FMA pipe): one per
+    plane and 32-word slab; even field widths fold their last plane into the
+    field OR instead (fpg_slice.cuh)."""
+    if exact:
+        return X_BITS * X_LEN / 32.0
+    v, w = scheme.variant().name, scheme.width()
+    fw = scheme.bits_per_count() if v == "Count" else scheme.bits_per_position() if v == "Position" else 1
+    extra = w % fw if v == "Position" else 0
+    nf = (w - extra) // fw
+    planes = nf * (fw - 1 if fw % 2 == 0 else fw) + extra + sig_fields
+    return planes / 32.0
+
+
 X_LEN, X_BITS = 6, 5  # the exact Hamming path of short words (fpg_kernels.cuh kXLen / kXBits)
 
 
@@ -548,12 +570,21 @@ def main():
             pairs_x * ops_per_comparison(w.scheme, shape["sig_fields"], exact=True)) /
            max(pairs_m + pairs_x, 1))
     lop3_clk, lop3_basis = alu_peak()
+    imad_clk = imad_peak()
+    imads = ((pairs_m * imads_per_comparison(w.scheme, shape["sig_fields"]) +
+              pairs_x * imads_per_comparison(w.scheme, shape["sig_fields"], exact=True)) / max(pairs_m + pairs_x, 1))
     popc_peak = sms * sm_mhz * 1e6 * POPC_PER_CLK_PER_SM / math.ceil(w.scheme.width() / 32) / 1e12
     if shape["sliced"]:
-        peak = sms * sm_mhz * 1e6 * lop3_clk / ops / 1e12
-        bound, basis = "int-alu", (f"{sms} SMs x {sm_mhz:.0f} MHz x {lop3_clk:.1f} LOP3/clk/SM ({lop3_basis}) / "
-                                   f"{ops:.3f} LOP3 per comparison (bit-sliced test, {shape['sig_fields']} sig' planes; "
-                                   f"exact-path pairs weighted with their own count)")
+        # the pipe that binds: the ALU pipe (LOP3: the counters) or the FMA pipe
+        # (IMAD: the query XOR of every plane); the position-code path has more
+        # IMAD (30 per 32 pairs) than LOP3 (24)
+        peak_alu = sms * sm_mhz * 1e6 * lop3_clk / ops / 1e12
+        peak_fma = sms * sm_mhz * 1e6 * imad_clk / max(imads, 1e-9) / 1e12
+        peak = min(peak_alu, peak_fma)
+        bound = "int-alu" if peak_alu <= peak_fma else "int-fma"
+        basis = (f"{sms} SMs x {sm_mhz:.0f} MHz x min({lop3_clk:.1f} LOP3/clk/SM / {ops:.3f} LOP3 per comparison, "
+                 f"{imad_clk:.1f} IMAD/clk/SM / {imads:.3f} IMAD per comparison) ({lop3_basis}; bit-sliced test, "
+                 f"{shape['sig_fields']} sig' planes; position-code-path pairs weighted with their own counts)")
     else:
         peak = popc_peak
         bound, basis = "int-xu", f"{sms} SMs x {sm_mhz:.0f} MHz x {POPC_PER_CLK_PER_SM} POPC/clk/SM / ceil(W/32)"
@@ -604,6 +635,7 @@ def main():
                      "pairs_basis": "pairs K2 evaluated (length-compatible minus weight-window skips)",
                      "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",
                      "peak_basis": basis,
+                     "peak_alu": peak_alu if shape["sliced"] else None, "peak_fma": peak_fma if shape["sliced"] else None,
                      "popc_equiv_peak": popc_peak, "popc_equiv_frac": achieved / popc_peak,
                      "filter_ms_per_launch": filt_avg_ms, "filter_share_of_step": filt_avg_ms / ms_per_step},
         "clocks": clk,

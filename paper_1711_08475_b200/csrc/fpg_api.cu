@@ -284,9 +284,9 @@ struct Collection {
     std::vector<uint64_t> plane_base;    // L1
     DBuf<uint32_t> planes;
     DBuf<uint32_t> wt;        // bit-sliced K2: group weights (fp_gweight) per sorted position
-    DBuf<uint32_t> xc;        // exact path: symbol codes of the first kXLen bytes (kXBits each)
-    DBuf<uint32_t> xplanes;   // exact path planes of the buckets L <= kXLen: fingerprint bits, then codes
-    std::vector<uint64_t> xplane_base;  // per length <= kXLen: u32 offset in xplanes
+    DBuf<uint32_t> xc;        // position path: symbol codes of kXLen byte positions (kXBits each)
+    DBuf<uint32_t> xplanes;   // position path planes (every bucket): the code planes
+    std::vector<uint64_t> xplane_base;  // per length: u32 offset in xplanes
     DBuf<uint64_t> d_xplane_base;
     DBuf<uint2> slab_w;       // bit-sliced dictionary: group-weight box (min, max nibbles) per global slab
     DBuf<uint2> gbox;         // ... and per slab group (32 * SL slabs of a bucket)
@@ -524,24 +524,25 @@ struct Collection {
                 ++launches;
             }
             if (P.xlen) {
-                // exact path planes (same kernel): fingerprint bits, then the
-                // position codes, for the buckets of words <= kXLen bytes
+                // position-code planes (same kernel), every bucket: the symbol codes
+                // of kXLen byte positions of each word (k_build: all positions of a
+                // word of <= kXLen bytes, else kXLen positions spread over the word)
                 const int xnpt = fpg::kXBits * fpg::kXLen;  // code planes only (QueryStats come from the histograms)
-                xplane_base.assign(fpg::kXLen + 1, 0);
+                xplane_base.assign(L1, 0);
                 uint64_t xb = 0;
-                for (int L = 0; L <= fpg::kXLen; ++L) {
+                for (int L = 0; L < L1; ++L) {
                     xplane_base[L] = xb;
                     xb += cdiv(cdiv(count[L], 32), 32) * 32 * (uint64_t)xnpt;
                 }
-                const uint32_t xsl = slab_start[fpg::kXLen + 1];
+                const uint32_t xsl = slab_start[L1];
                 if (xsl) {
                     xplanes.reserve(xb);
-                    d_xplane_base.reserve(fpg::kXLen + 1);
-                    CK(cudaMemcpyAsync(d_xplane_base.p, xplane_base.data(), sizeof(uint64_t) * (fpg::kXLen + 1),
-                                       cudaMemcpyHostToDevice, st));
+                    d_xplane_base.reserve(L1);
+                    CK(cudaMemcpyAsync(d_xplane_base.p, xplane_base.data(), sizeof(uint64_t) * L1, cudaMemcpyHostToDevice,
+                                       st));
                     fpg::k_planes<<<(unsigned)cdiv(xsl, fpg::kPlanesSlabs), 32 * fpg::kPlanesSlabs, 0, st>>>(
-                        fp.p, xc.p, nullptr, nullptr, d_slab_start.p, d_start.p, d_count.p, d_xplane_base.p,
-                        fpg::kXLen + 1, xsl, 0, xnpt, xplanes.p);
+                        fp.p, xc.p, nullptr, nullptr, d_slab_start.p, d_start.p, d_count.p, d_xplane_base.p, L1, xsl, 0,
+                        xnpt, xplanes.p);
                     CK(cudaGetLastError());
                     ++launches;
                 }
@@ -958,7 +959,7 @@ void run_shard(fpg_dict* D, fpg_batch* B, ShardBatch& S, const fpg_query_options
                     t.count_only = count_only ? 1u : 0u;
                     t.slab_g0 = W.slab_start[lw];
                     t.gbox_base = W.group_start[lw] + s0 / grp;
-                    const bool xt = xpath && lw <= fpg::kXLen && !count_only;
+                    const bool xt = xpath && !count_only;  // every length: exact up to kXLen bytes, a position filter beyond
                     if (xt) t.plane_base = W.xplane_base[lw];
                     (xt ? splan_x : splan).push_back(t);
                 }

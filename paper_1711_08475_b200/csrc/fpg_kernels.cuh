@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(256) k_build(const uint8_t* __restrict__ blob,
     uint8_t* dst = bytes_out ? bytes_out + bucket_bytes[len] + (uint64_t)(pos - bucket_start[len]) * stride : nullptr;
     FpBuilder<VARIANT> fb;
     fb.init(P);
-    uint32_t sig = 0, sigp = 0, xc = 0;  // xc: position codes of the first kXLen bytes (exact path)
+    uint32_t sig = 0, sigp = 0, xc = 0;  // xc: symbol codes of kXLen byte positions (exact / position path)
     for (int c = 0; c < stride; c += 16) {
         uint32_t w[4];
         const int rem = min(16, len - c);
@@ -275,7 +275,21 @@ __global__ void __launch_bounds__(256) k_build(const uint8_t* __restrict__ blob,
                 sig |= 1u << (byte & 31);
                 const int g = s_sigbit[byte];
                 if (g >= 0) sigp |= 1u << g;
-                if (c + t < kXLen) xc |= (uint32_t)s_xcode[byte] << (kXBits * (c + t));
+            }
+        }
+        // position codes (K2's exact / position path): every byte of a word of
+        // <= kXLen bytes, else the kXLen positions floor(j * len / kXLen),
+        // j = 0 .. kXLen - 1 (spread over the word; words and queries of one
+        // length pick the same positions)
+        if (xc_out) {
+#pragma unroll
+            for (int j = 0; j < kXLen; ++j) {
+                const int p = len <= kXLen ? j : (j * len) / kXLen;
+                if (p < len && p >= c && p < c + 16) {
+                    const int o = p - c;
+                    const uint32_t wv = (o >> 2) == 0 ? w[0] : (o >> 2) == 1 ? w[1] : (o >> 2) == 2 ? w[2] : w[3];
+                    xc |= (uint32_t)s_xcode[(wv >> (8 * (o & 3))) & 0xffu] << (kXBits * j);
+                }
             }
         }
     }
