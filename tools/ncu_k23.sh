@@ -5,7 +5,8 @@ tag=$1; cfg=$2; cell=$3; shift 3
 o=gpurun_out/$tag; mkdir -p $o
 run="python bench.py --config $cfg --cell $cell --no-cpu-baseline --no-e2e --steps 1 --warmup 1"
 for k in ${KERNELS:-k_verify k_slice}; do
-  re=$k; [ $k = k_slice ] && re='k_slice.*bool.0, .bool.0>'
+  # default: the sig' launch (X = 0, NB = 0); KREGEX=k_slice takes the batch's second K2 launch whatever it is
+  re=$k; [ $k = k_slice ] && re=${KREGEX:-'k_slice.*bool.0, .bool.0>'}
   env "$@" timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$re" -s 1 -c 1 -o $o/$k $run > $o/ncu_$k.log 2>&1
   echo ${k}_ncu_rc=$?
   python tools/ncu_summary.py report $o/$k.ncu-rep 40 > $o/${k}_summary.txt 2>&1
