@@ -215,8 +215,9 @@ int fpg_batch_last_verify(const fpg_batch* batch, int32_t shard, double* verify_
  * more than 2k apart (L1 distance over 4 field groups <= F_D, so they are
  * rejected). */
 int fpg_batch_last_scanned(const fpg_batch* batch, int32_t shard, uint64_t* scanned);
-/* Of those, the pairs evaluated by the exact Hamming path of short words
- * (position-code planes instead of sig'; 0 when the run had none). */
+/* Of those, the pairs evaluated by the position-code path (Hamming over
+ * 16-bit schemes and small alphabets: position-code planes instead of
+ * fingerprint and sig' planes; 0 when the run had none). */
 int fpg_batch_last_scanned_exact(const fpg_batch* batch, int32_t shard, uint64_t* scanned);
 
 #ifdef __cplusplus

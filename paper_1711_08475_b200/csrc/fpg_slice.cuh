@@ -216,13 +216,15 @@ __device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
 // uniform branches on them; other runs take the generic instantiation
 // (HOT = false), which reads them from P.
 //
-// X (exact Hamming path, words of <= kXLen bytes; instantiated with NP = 0):
-// the planes are the words' symbol codes, kXBits planes per byte position,
-// and q_sigp holds the queries' codes.  The counters count the positions
-// whose codes differ, and a word is a candidate iff at most k positions
-// differ: exactly hamming_bounded's test (edit_distance.hpp:18-27), so the
-// verifier sees only true matches.  No scheme planes, no survivor counters:
-// the host takes the path only when QueryStats come from the histograms.
+// X (position-code path, Hamming; instantiated with NP = 0): the planes are
+// the symbol codes of kXLen byte positions of each word, kXBits planes per
+// position (every position of a word of <= kXLen bytes, else positions spread
+// over the word, k_build), and q_sigp holds the queries' codes.  The counters
+// count the positions whose codes differ, and a word is a candidate iff at
+// most k of them differ: exactly hamming_bounded's test
+// (edit_distance.hpp:18-27) for words of <= kXLen bytes, a sound filter for
+// longer ones (K3 decides).  No scheme planes, no survivor counters: the host
+// takes the path only when QueryStats come from the histograms.
 template <int NP, int FW, int EXTRA, int S, bool HOT, bool X = false, bool NB = false>
 __global__ void __launch_bounds__(kSliceThreads, 2) k_slice(const SliceTile* __restrict__ tiles, uint32_t ntiles,
                                                             const __grid_constant__ SliceParams P) {
